@@ -1,0 +1,144 @@
+/*
+ * fda.h -- C ABI of the B200 FDA Burton-Miller apply (libfda.so).
+ *
+ * The library applies the Nystrom-discretised Burton-Miller operator H of
+ * Cao, Wen, Xiao & Liu (arXiv 1311.5202) with the fast directional algorithm:
+ *
+ *   out_i = sum_{j != i} w_j K(x_i, n_i; x_j, n_j) phi_j + sum_{p in row i} val_p phi_{col_p}
+ *
+ *   K = dG/dn_y + alpha d2G/(dn_x dn_y),  G = e^{ikr}/(4 pi r)      PAPER.md:352-355 (eq_hmat), 210-212
+ *   far quadrature w_j K(x_i, y_j)                                  PAPER.md:291-297 (eq:far field)
+ *   locally corrected kernel K-bar inside D_i, supplied by the caller
+ *   as a delta CSR (the "val" term)                                 PAPER.md:329-341 (eq:sum, kcorrection)
+ *
+ * The first term is approximated by the FDA (near-field P2P + S2M / M2M /
+ * M2L / L2L / L2T) to the accuracy eps;
+ * the CSR term is exact.  Targets are the sources themselves (Nystrom
+ * collocation).  Everything of the apply runs in this library's CUDA kernels
+ * (sm_100a); there is no CPU fallback: without a CUDA device every call that
+ * needs one returns FDA_ERR_CUDA.
+ *
+ * Layout and ownership
+ *   points, normals : n x 3 doubles, xyz interleaved, caller order; normals unit, outward.
+ *   quad_weights    : n doubles, > 0 (rule weight x Jacobian).
+ *   phi, out        : n complex128 (2n doubles, re/im interleaved), caller order.
+ *   Any array argument may be host memory (pageable or pinned) or device memory
+ *   of the current device; the library detects which (cudaPointerGetAttributes).
+ *   fda_plan_create / fda_plan_set_correction COPY their inputs: the caller may
+ *   free them on return.  The plan owns all device workspace.
+ *
+ * Errors: every function returns an fda_status; nothing throws across the ABI.
+ *   FDA_ERR_INVALID_ARG   bad sizes / null pointers / non-finite values / |n| != 1 (1e-10) /
+ *                         w <= 0 / eps not in [1e-10, 1e-1] / k < 0 / (k == 0 and alpha != 0) /
+ *                         CSR with non-monotone row_ptr or col outside [0, n)
+ *   FDA_ERR_COINCIDENT_POINTS  two distinct points closer than 1e-14 x root width
+ *   FDA_ERR_ALIAS         phi and out are the same buffer
+ *   FDA_ERR_CUDA          a CUDA error (sticky: destroy the plan)
+ *   FDA_ERR_OOM           device allocation failed
+ * Threading: one apply in flight per plan; the device-pointer apply is ordered on
+ * the plan's stream (fda_plan_set_stream) and does not synchronise the host.
+ */
+#ifndef FDA_H
+#define FDA_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fda_plan_s* fda_plan;
+
+typedef enum {
+  FDA_OK = 0,
+  FDA_ERR_INVALID_ARG = 1,
+  FDA_ERR_COINCIDENT_POINTS = 2,
+  FDA_ERR_ALIAS = 3,
+  FDA_ERR_CUDA = 4,
+  FDA_ERR_OOM = 5,
+  FDA_ERR_SETUP_ACCURACY = 6,
+  FDA_ERR_NCCL = 7,
+  FDA_ERR_STATE = 8
+} fda_status;
+
+/* phase mask for fda_apply_phases (tests / diagnostics) */
+#define FDA_PHASE_NEAR 1u /* P2P over the plan's near leaf pairs (H2)             */
+#define FDA_PHASE_CORR 2u /* correction CSR (H3)                                   */
+#define FDA_PHASE_FAR 4u  /* S2M, M2M, M2L, L2L, L2T (H4-H8)                        */
+#define FDA_PHASE_ALL 7u
+
+/* Plan knobs (all optional; fda_options_default fills the defaults). */
+typedef struct {
+  int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
+  double eps_internal;     /* truncation tolerance of every SVD / ID; 0 -> eps / 100 (R11) */
+  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6) */
+  int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths (default 8) */
+  double lf_p_switch;      /* w / lambda switch (default 0.5) */
+  int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */
+  int32_t single_leaf;     /* debug: no far field, every pair P2P (default 0) */
+  int32_t hf_max_rows;     /* HF directional-set sample rows (default 6000) */
+  double hf_spacing;       /* HF candidate spacing in wavelengths (default 0.25) */
+  int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1) */
+  int32_t verbose;         /* plan log (fda_plan_log) */
+  int32_t host_only;       /* diagnostics: build the host plan only (tree, lists, operators), no device;
+                              fda_apply* then returns FDA_ERR_STATE.  Lets CPU tests audit the lists. */
+} fda_options;
+
+typedef struct {
+  int64_t n, nleaves, nlevels, lmin;
+  int64_t p2p_leaf_pairs, p2p_point_pairs;
+  int64_t m2l_pairs, m2l_groups, m2l_lowrank_groups;
+  int64_t out_slots, in_slots;
+  int64_t csr_nnz;
+  int64_t device_bytes;
+  int64_t owned_begin, owned_end; /* owned points, Morton order */
+  double setup_tree_s, setup_lists_s, setup_ops_s, setup_upload_s;
+  double flops_p2p, flops_m2l, flops_m2m, flops_l2l, flops_s2m, flops_l2t; /* algorithmic flops per apply */
+  double bytes_csr;                                                        /* algorithmic bytes of H3 per apply */
+} fda_stats;
+
+void fda_options_default(fda_options* opt);
+
+/* Build a plan (tree, lists, wedges, translation operators) and upload it.
+ * k >= 0 wavenumber; alpha = alpha_re + i alpha_im (Burton-Miller coupling, i/k in the paper);
+ * eps in [1e-10, 1e-1] target accuracy of the far field. */
+fda_status fda_plan_create(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                           double k, double alpha_re, double alpha_im, double eps, fda_plan* out);
+fda_status fda_plan_create_ex(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                              double k, double alpha_re, double alpha_im, double eps, const fda_options* opt,
+                              fda_plan* out);
+
+/* Singular-correction CSR in caller order: row_ptr (n+1, int64, row_ptr[0] = 0, monotone, row_ptr[n] = nnz),
+ * col (nnz, int32 in [0,n)), val (nnz complex128, interleaved).  Copied into the plan (Morton order).
+ * nnz = 0 removes it. */
+fda_status fda_plan_set_correction(fda_plan plan, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                                   const double* val);
+
+/* out = H phi.  phi / out: n complex128 each, caller order, host or device. */
+fda_status fda_apply(fda_plan plan, const double* phi, double* out);
+/* Same, restricted to the phases in mask (FDA_PHASE_*). */
+fda_status fda_apply_phases(fda_plan plan, uint32_t mask, const double* phi, double* out);
+/* Same as fda_apply_phases, with CUDA-event time per phase written to phase_ms[0..8]:
+ * permute, p2p, csr, s2m, m2m, m2l, l2l, l2t, unpermute (device pointers only; synchronises). */
+fda_status fda_apply_timed(fda_plan plan, uint32_t mask, const double* phi, double* out, float* phase_ms);
+
+/* Order the plan's device work on this cudaStream_t (default: the legacy default stream). */
+fda_status fda_plan_set_stream(fda_plan plan, void* stream);
+fda_status fda_plan_stats(fda_plan plan, fda_stats* stats);
+const char* fda_plan_log(fda_plan plan);
+
+/* Diagnostics for the list audit (host arrays; pass NULL arrays to query sizes).
+ * leaf_of_point: n (caller order); leaf_level / leaf_ijk: per leaf (ijk: 3 int64). */
+fda_status fda_plan_export_leaves(fda_plan plan, int64_t* nleaves, int32_t* leaf_of_point, int32_t* leaf_level,
+                                  int64_t* leaf_ijk);
+/* The exact (target leaf, source leaf) pairs the P2P phase sums. */
+fda_status fda_plan_export_p2p(fda_plan plan, int64_t* npairs, int32_t* tgt_leaf, int32_t* src_leaf);
+/* The M2L cube pairs: level, target cube ijk (3), source cube ijk (3). */
+fda_status fda_plan_export_m2l(fda_plan plan, int64_t* npairs, int32_t* level, int64_t* tgt_ijk, int64_t* src_ijk);
+
+fda_status fda_plan_destroy(fda_plan plan);
+const char* fda_status_str(fda_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDA_H */

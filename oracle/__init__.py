@@ -27,7 +27,7 @@ KIND_G, KIND_DNY, KIND_DNX, KIND_HYP, KIND_BMH, KIND_BMG = range(6)
 def build():
     so = os.path.join(_HERE, "liboracle.so")
     src = os.path.join(_HERE, "oracle.c")
-    subprocess.check_call(["gcc", "-O3", "-march=native", "-fopenmp", "-fno-fast-math", "-shared",
+    subprocess.check_call(["gcc", "-O3", "-march=x86-64-v3", "-fopenmp", "-fno-fast-math", "-shared",
                            "-fPIC", src, "-o", so + ".tmp", "-lm"])
     os.replace(so + ".tmp", so)
 

@@ -1,0 +1,647 @@
+// api.cu -- the C ABI (include/fda.h): plan upload, apply orchestration, diagnostics.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/fda.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using fda::cplx;
+
+namespace {
+
+struct DevLevel {
+  int s = 0;
+  int64_t n_out = 0, n_in = 0;
+  double2* X = nullptr;
+  double2* Y = nullptr;
+  // M2L
+  int64_t ngroups = 0;
+  int64_t *gbeg = nullptr, *gend = nullptr, *gmat = nullptr;
+  int32_t* grank = nullptr;
+  double2* pool = nullptr;
+};
+struct DevTrans {
+  int lp = 0, sp = 0, sc = 0;
+  double2 *pool = nullptr, *poolT = nullptr;
+  int64_t n_par = 0, n_child = 0;
+  int64_t *up_ptr = nullptr, *dn_ptr = nullptr;
+  int32_t *up_child = nullptr, *up_mat = nullptr, *dn_parent = nullptr, *dn_mat = nullptr;
+};
+struct DevLeafOps {
+  int level = 0, s = 0, nsurf = 0;
+  int64_t nleaves = 0;       // all leaves of the level (S2M)
+  int64_t nleaves_own = 0;   // owned leaves (L2T) -- first nleaves_own of the l2t arrays
+  int32_t *leaf = nullptr, *slot = nullptr;
+  int32_t *leaf_own = nullptr, *slot_own = nullptr;
+  double* surf = nullptr;
+  double2 *S = nullptr, *T = nullptr;
+};
+
+}  // namespace
+
+struct fda_plan_s {
+  fda::HostPlan H;
+  int dev = 0;
+  cudaStream_t stream = 0;
+  bool sticky_error = false;
+  bool host_only = false;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  // geometry
+  int64_t n = 0, nleaf = 0;
+  double *px, *py, *pz, *nx, *ny, *nz, *w;
+  int32_t* perm;
+  int64_t* leaf_ptr;
+  double *lcx, *lcy, *lcz;
+  int64_t *p2p_ptr;
+  int32_t* p2p_src;
+  double2 *q, *phim, *outm, *phi_buf, *out_buf;
+  // ownership (multi-GPU)
+  int64_t leaf_b = 0, leaf_e = 0, pt_b = 0, pt_e = 0;
+  // correction
+  int64_t nnz = 0;
+  int64_t* c_ptr = nullptr;
+  int32_t* c_col = nullptr;
+  double2* c_val = nullptr;
+  // far field
+  std::vector<DevLevel> lv;
+  std::vector<DevTrans> tr;
+  std::vector<DevLeafOps> lo;
+  int32_t *m2l_tgt = nullptr, *m2l_src = nullptr;
+  fda_stats st{};
+  std::string logstr;
+};
+
+namespace {
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct CudaFail {
+  fda_status s;
+};
+
+void ck(cudaError_t e) {
+  if (e == cudaErrorMemoryAllocation) throw CudaFail{FDA_ERR_OOM};
+  if (e != cudaSuccess) throw CudaFail{FDA_ERR_CUDA};
+}
+
+template <class T>
+T* dalloc(fda_plan P, size_t count) {
+  if (count == 0) count = 1;
+  void* p = nullptr;
+  ck(cudaMalloc(&p, count * sizeof(T)));
+  P->allocs.push_back(p);
+  P->bytes += (int64_t)(count * sizeof(T));
+  return (T*)p;
+}
+template <class T>
+T* upload(fda_plan P, const T* h, size_t count) {
+  T* d = dalloc<T>(P, count);
+  if (count) ck(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+template <class T>
+T* upload(fda_plan P, const std::vector<T>& v) {
+  return upload(P, v.data(), v.size());
+}
+int32_t* upload_i32(fda_plan P, const std::vector<int64_t>& v) {
+  std::vector<int32_t> t(v.begin(), v.end());
+  return upload(P, t);
+}
+double2* upload_c(fda_plan P, const std::vector<cplx>& v) {
+  return upload(P, reinterpret_cast<const double2*>(v.data()), v.size());
+}
+
+// copy an input array (host or device) to a host vector
+template <class T>
+std::vector<T> to_host(const T* p, size_t count) {
+  std::vector<T> h(count);
+  if (!count) return h;
+  if (is_device_ptr(p)) ck(cudaMemcpy(h.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost));
+  else std::memcpy(h.data(), p, count * sizeof(T));
+  return h;
+}
+
+void free_plan(fda_plan P) {
+  for (void* p : P->allocs) cudaFree(p);
+  P->allocs.clear();
+}
+
+fda_status upload_plan(fda_plan P, const fda_options& o) {
+  fda::HostPlan& H = P->H;
+  const int64_t n = H.n;
+  P->n = n;
+  P->px = upload(P, H.px), P->py = upload(P, H.py), P->pz = upload(P, H.pz);
+  P->nx = upload(P, H.nx), P->ny = upload(P, H.ny), P->nz = upload(P, H.nz);
+  P->w = upload(P, H.w);
+  P->perm = upload(P, H.perm);
+  const int64_t nl = (int64_t)H.leaves.size();
+  P->nleaf = nl;
+  std::vector<int64_t> lp(nl + 1);
+  std::vector<double> cx(nl), cy(nl), cz(nl);
+  for (int64_t t = 0; t < nl; ++t) {
+    const fda::Cube& c = H.cubes[H.leaves[t]];
+    lp[t] = c.pbeg;
+    lp[t + 1] = c.pend;
+    const double wl = H.root_w / (double)(1LL << c.level);
+    cx[t] = H.root_lo[0] + (c.ijk[0] + 0.5) * wl;
+    cy[t] = H.root_lo[1] + (c.ijk[1] + 0.5) * wl;
+    cz[t] = H.root_lo[2] + (c.ijk[2] + 0.5) * wl;
+  }
+  P->leaf_ptr = upload(P, lp);
+  P->lcx = upload(P, cx), P->lcy = upload(P, cy), P->lcz = upload(P, cz);
+  P->p2p_ptr = upload(P, H.p2p_ptr);
+  P->p2p_src = upload_i32(P, H.p2p_src);
+  P->q = dalloc<double2>(P, n), P->phim = dalloc<double2>(P, n), P->outm = dalloc<double2>(P, n);
+  P->phi_buf = dalloc<double2>(P, n), P->out_buf = dalloc<double2>(P, n);
+  // ownership: contiguous leaf range balanced by points (multi-GPU)
+  const int R = std::max(1, o.nranks), r = std::min(std::max(0, o.rank), R - 1);
+  {
+    const int64_t pb = (n * r) / R, pe = (n * (r + 1)) / R;
+    int64_t lb = std::lower_bound(lp.begin(), lp.begin() + nl, pb) - lp.begin();
+    int64_t le = std::lower_bound(lp.begin(), lp.begin() + nl, pe) - lp.begin();
+    if (r == R - 1) le = nl;
+    if (r == 0) lb = 0;
+    P->leaf_b = lb, P->leaf_e = le;
+    P->pt_b = lp[lb], P->pt_e = lp[le];
+  }
+  auto owned_cube = [&](int64_t gid) {
+    const fda::Cube& c = H.cubes[gid];
+    return c.pend > P->pt_b && c.pbeg < P->pt_e;
+  };
+  // levels
+  const int nlev = (int)H.levels.size();
+  P->lv.assign(nlev, DevLevel());
+  for (int l = 0; l < nlev; ++l) {
+    const fda::Level& L = H.levels[l];
+    DevLevel& D = P->lv[l];
+    D.s = L.s, D.n_out = L.n_out, D.n_in = L.n_in;
+    if (L.n_out) D.X = dalloc<double2>(P, (size_t)L.n_out * L.s);
+    if (L.n_in) D.Y = dalloc<double2>(P, (size_t)L.n_in * L.s);
+  }
+  // M2L groups: filter pairs to owned targets
+  {
+    std::vector<int64_t> tg, sr;
+    for (int l = 0; l < nlev; ++l) {
+      const fda::Level& L = H.levels[l];
+      DevLevel& D = P->lv[l];
+      std::vector<int64_t> gb, ge, gm;
+      std::vector<int32_t> gr;
+      for (const auto& G : H.m2l_groups) {
+        if (G.level != l) continue;
+        const int64_t b0 = (int64_t)tg.size();
+        for (int64_t p = G.pbeg; p < G.pend; ++p) {
+          const int64_t ts = H.m2l_tgt[p];
+          if (R > 1 && !owned_cube(L.cubes[L.in_cube[ts]])) continue;
+          tg.push_back(ts);
+          sr.push_back(H.m2l_src[p]);
+        }
+        if ((int64_t)tg.size() == b0) continue;
+        gb.push_back(b0), ge.push_back((int64_t)tg.size()), gm.push_back(G.mat_off), gr.push_back(G.rank);
+        P->st.m2l_pairs += (int64_t)tg.size() - b0;
+        P->st.m2l_groups += 1;
+        P->st.m2l_lowrank_groups += G.rank >= 0;
+        const double np = (double)((int64_t)tg.size() - b0);
+        P->st.flops_m2l += np * (G.rank < 0 ? 8.0 * L.s * L.s : 16.0 * G.rank * L.s);
+      }
+      D.ngroups = (int64_t)gb.size();
+      if (D.ngroups) {
+        D.gbeg = upload(P, gb), D.gend = upload(P, ge), D.gmat = upload(P, gm), D.grank = upload(P, gr);
+        D.pool = upload_c(P, H.m2l_pool[l]);
+      }
+    }
+    P->m2l_tgt = upload_i32(P, tg);
+    P->m2l_src = upload_i32(P, sr);
+  }
+  // transitions
+  for (const auto& T : H.trans) {
+    DevTrans D;
+    D.lp = T.lp, D.sp = T.sp, D.sc = T.sc;
+    D.pool = upload_c(P, T.pool);
+    D.poolT = upload_c(P, T.poolT);
+    D.n_par = (int64_t)T.up_ptr.size() - 1;
+    D.n_child = (int64_t)T.dn_ptr.size() - 1;
+    std::vector<int64_t> um(T.up_mat.size()), dm(T.dn_mat.size());
+    for (size_t e = 0; e < um.size(); ++e) um[e] = T.mat_index[T.up_mat[e]];
+    for (size_t e = 0; e < dm.size(); ++e) dm[e] = T.mat_index[T.dn_mat[e]];
+    D.up_ptr = upload(P, T.up_ptr), D.up_child = upload_i32(P, T.up_child), D.up_mat = upload_i32(P, um);
+    D.dn_ptr = upload(P, T.dn_ptr), D.dn_parent = upload_i32(P, T.dn_parent), D.dn_mat = upload_i32(P, dm);
+    P->st.flops_m2m += 8.0 * T.sp * T.sc * (double)T.up_child.size();
+    P->st.flops_l2l += 8.0 * T.sp * T.sc * (double)T.dn_parent.size();
+    P->tr.push_back(D);
+  }
+  // leaf operators
+  for (const auto& O : H.leafops) {
+    const fda::Level& L = H.levels[O.level];
+    DevLeafOps D;
+    D.level = O.level, D.s = L.s, D.nsurf = L.nsurf;
+    D.nleaves = (int64_t)O.leaf.size();
+    D.leaf = upload_i32(P, O.leaf), D.slot = upload_i32(P, O.slot);
+    std::vector<int64_t> lo_, so_;
+    for (size_t t = 0; t < O.leaf.size(); ++t)
+      if (O.leaf[t] >= P->leaf_b && O.leaf[t] < P->leaf_e) lo_.push_back(O.leaf[t]), so_.push_back(O.slot[t]);
+    D.nleaves_own = (int64_t)lo_.size();
+    D.leaf_own = upload_i32(P, lo_), D.slot_own = upload_i32(P, so_);
+    std::vector<double> sf;
+    for (const auto& p : L.ck_pts) sf.insert(sf.end(), {p[0], p[1], p[2]});
+    D.surf = upload(P, sf);
+    D.S = upload_c(P, O.S);
+    D.T = upload_c(P, O.T);
+    for (int64_t t = 0; t < D.nleaves; ++t) {
+      const double npt = (double)(lp[O.leaf[t] + 1] - lp[O.leaf[t]]);
+      P->st.flops_s2m += npt * L.nsurf * 40.0 + 8.0 * L.s * L.nsurf;
+    }
+    for (size_t t = 0; t < lo_.size(); ++t) {
+      const double npt = (double)(lp[lo_[t] + 1] - lp[lo_[t]]);
+      P->st.flops_l2t += npt * L.nsurf * 45.0 + 8.0 * L.s * L.nsurf;
+    }
+    P->lo.push_back(D);
+  }
+  // stats
+  fda_stats& s = P->st;
+  s.n = n;
+  s.nleaves = nl;
+  s.nlevels = nlev;
+  s.lmin = H.lmin;
+  s.p2p_leaf_pairs = (int64_t)H.p2p_src.size();
+  for (int64_t t = P->leaf_b; t < P->leaf_e; ++t)
+    for (int64_t e = H.p2p_ptr[t]; e < H.p2p_ptr[t + 1]; ++e)
+      s.p2p_point_pairs += (lp[t + 1] - lp[t]) * (lp[H.p2p_src[e] + 1] - lp[H.p2p_src[e]]);
+  s.flops_p2p = 100.0 * (double)s.p2p_point_pairs;
+  for (int l = 0; l < nlev; ++l) s.out_slots += H.levels[l].n_out, s.in_slots += H.levels[l].n_in;
+  s.owned_begin = P->pt_b, s.owned_end = P->pt_e;
+  s.setup_tree_s = H.t_tree, s.setup_lists_s = H.t_lists, s.setup_ops_s = H.t_ops;
+  return FDA_OK;
+}
+
+bool finite3(const std::vector<double>& v) {
+  for (double x : v)
+    if (!std::isfinite(x)) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+void fda_options_default(fda_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  fda::Options d;
+  o->leaf_size = 0;
+  o->eps_internal = 0;
+  o->lf_p_low = d.lf_p_low;
+  o->lf_p_high = d.lf_p_high;
+  o->lf_p_switch = d.lf_p_switch;
+  o->lowrank = 1;
+  o->single_leaf = 0;
+  o->hf_max_rows = d.hf_max_rows;
+  o->hf_spacing = d.hf_spacing;
+  o->rank = 0;
+  o->nranks = 1;
+  o->verbose = 0;
+}
+
+const char* fda_status_str(fda_status s) {
+  switch (s) {
+    case FDA_OK: return "FDA_OK";
+    case FDA_ERR_INVALID_ARG: return "FDA_ERR_INVALID_ARG";
+    case FDA_ERR_COINCIDENT_POINTS: return "FDA_ERR_COINCIDENT_POINTS";
+    case FDA_ERR_ALIAS: return "FDA_ERR_ALIAS";
+    case FDA_ERR_CUDA: return "FDA_ERR_CUDA";
+    case FDA_ERR_OOM: return "FDA_ERR_OOM";
+    case FDA_ERR_SETUP_ACCURACY: return "FDA_ERR_SETUP_ACCURACY";
+    case FDA_ERR_NCCL: return "FDA_ERR_NCCL";
+    case FDA_ERR_STATE: return "FDA_ERR_STATE";
+  }
+  return "FDA_ERR_UNKNOWN";
+}
+
+fda_status fda_plan_create_ex(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                              double k, double alpha_re, double alpha_im, double eps, const fda_options* opt,
+                              fda_plan* out) {
+  if (!out) return FDA_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n < 1 || !points || !normals || !quad_weights) return FDA_ERR_INVALID_ARG;
+  if (!std::isfinite(k) || k < 0 || !std::isfinite(alpha_re) || !std::isfinite(alpha_im)) return FDA_ERR_INVALID_ARG;
+  if (k == 0 && (alpha_re != 0 || alpha_im != 0)) return FDA_ERR_INVALID_ARG;
+  if (!(eps >= 1e-10 && eps <= 1e-1)) return FDA_ERR_INVALID_ARG;
+  if (n > (int64_t)INT32_MAX) return FDA_ERR_INVALID_ARG;
+  fda_options o;
+  fda_options_default(&o);
+  if (opt) o = *opt;
+  int ndev = 0;
+  if (!o.host_only && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)) {
+    cudaGetLastError();
+    return FDA_ERR_CUDA;
+  }
+  std::unique_ptr<fda_plan_s> P(new fda_plan_s());
+  try {
+    if (!o.host_only) cudaGetDevice(&P->dev);
+    std::vector<double> x = to_host(points, (size_t)n * 3), nr = to_host(normals, (size_t)n * 3),
+                        w = to_host(quad_weights, (size_t)n);
+    if (!finite3(x) || !finite3(nr) || !finite3(w)) return FDA_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < n; ++i) {
+      const double nn = std::sqrt(nr[3 * i] * nr[3 * i] + nr[3 * i + 1] * nr[3 * i + 1] + nr[3 * i + 2] * nr[3 * i + 2]);
+      if (std::fabs(nn - 1.0) > 1e-10 || !(w[i] > 0)) return FDA_ERR_INVALID_ARG;
+    }
+    fda::Options fo;
+    fo.np = o.leaf_size;
+    fo.eps_int = o.eps_internal;
+    if (o.lf_p_low > 1) fo.lf_p_low = o.lf_p_low;
+    if (o.lf_p_high > 1) fo.lf_p_high = o.lf_p_high;
+    if (o.lf_p_switch > 0) fo.lf_p_switch = o.lf_p_switch;
+    fo.lowrank = o.lowrank;
+    fo.single_leaf = o.single_leaf;
+    if (o.hf_max_rows > 0) fo.hf_max_rows = o.hf_max_rows;
+    if (o.hf_spacing > 0) fo.hf_spacing = o.hf_spacing;
+    fo.verbose = o.verbose;
+    std::string err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo);
+    if (err == "COINCIDENT_POINTS") return FDA_ERR_COINCIDENT_POINTS;
+    if (!err.empty()) return FDA_ERR_INVALID_ARG;
+    P->host_only = o.host_only != 0;
+    P->logstr = P->H.log;
+    if (P->host_only) {
+      *out = P.release();
+      return FDA_OK;
+    }
+    const double t0 = now();
+    fda_status s = upload_plan(P.get(), o);
+    if (s != FDA_OK) {
+      free_plan(P.get());
+      return s;
+    }
+    ck(cudaDeviceSynchronize());
+    P->st.setup_upload_s = now() - t0;
+    P->st.device_bytes = P->bytes;
+    P->logstr = P->H.log;
+    // the host copies of the big pools are no longer needed
+    std::vector<std::vector<cplx>>().swap(P->H.m2l_pool);
+    for (auto& T : P->H.trans) std::vector<cplx>().swap(T.pool), std::vector<cplx>().swap(T.poolT);
+  } catch (const CudaFail& f) {
+    free_plan(P.get());
+    cudaGetLastError();
+    return f.s;
+  } catch (const std::bad_alloc&) {
+    free_plan(P.get());
+    return FDA_ERR_OOM;
+  }
+  *out = P.release();
+  return FDA_OK;
+}
+
+fda_status fda_plan_create(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                           double k, double alpha_re, double alpha_im, double eps, fda_plan* out) {
+  return fda_plan_create_ex(n, points, normals, quad_weights, k, alpha_re, alpha_im, eps, nullptr, out);
+}
+
+fda_status fda_plan_set_stream(fda_plan P, void* stream) {
+  if (!P) return FDA_ERR_INVALID_ARG;
+  P->stream = (cudaStream_t)stream;
+  return FDA_OK;
+}
+
+fda_status fda_plan_set_correction(fda_plan P, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                                   const double* val) {
+  if (!P) return FDA_ERR_INVALID_ARG;
+  if (P->host_only) return FDA_ERR_STATE;
+  if (P->sticky_error) return FDA_ERR_CUDA;
+  if (nnz < 0) return FDA_ERR_INVALID_ARG;
+  if (nnz > 0 && (!row_ptr || !col || !val)) return FDA_ERR_INVALID_ARG;
+  try {
+    if (P->c_ptr) {
+      // release the old correction
+      for (void* p : {(void*)P->c_ptr, (void*)P->c_col, (void*)P->c_val}) {
+        auto it = std::find(P->allocs.begin(), P->allocs.end(), p);
+        if (it != P->allocs.end()) P->allocs.erase(it);
+        cudaFree(p);
+      }
+      P->c_ptr = nullptr, P->c_col = nullptr, P->c_val = nullptr, P->nnz = 0;
+    }
+    if (nnz == 0) return FDA_OK;
+    const int64_t n = P->n;
+    std::vector<int64_t> rp = to_host(row_ptr, (size_t)n + 1);
+    if (rp[0] != 0 || rp[n] != nnz) return FDA_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < n; ++i)
+      if (rp[i + 1] < rp[i]) return FDA_ERR_INVALID_ARG;
+    std::vector<int32_t> cl = to_host(col, (size_t)nnz);
+    for (int64_t p = 0; p < nnz; ++p)
+      if (cl[p] < 0 || cl[p] >= n) return FDA_ERR_INVALID_ARG;
+    std::vector<double> vl = to_host(val, (size_t)nnz * 2);
+    // permute into Morton order: row m = caller row perm[m]; columns through the inverse permutation
+    const std::vector<int32_t>& perm = P->H.perm;
+    std::vector<int32_t> inv(n);
+    for (int64_t m = 0; m < n; ++m) inv[perm[m]] = (int32_t)m;
+    std::vector<int64_t> mp(n + 1, 0);
+    for (int64_t m = 0; m < n; ++m) mp[m + 1] = mp[m] + (rp[perm[m] + 1] - rp[perm[m]]);
+    std::vector<int32_t> mc(nnz);
+    std::vector<double> mv((size_t)nnz * 2);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t m = 0; m < n; ++m) {
+      const int64_t i = perm[m];
+      int64_t o = mp[m];
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p, ++o) {
+        mc[o] = inv[cl[p]];
+        mv[2 * o] = vl[2 * p];
+        mv[2 * o + 1] = vl[2 * p + 1];
+      }
+    }
+    P->c_ptr = upload(P, mp);
+    P->c_col = upload(P, mc);
+    P->c_val = upload(P, reinterpret_cast<const double2*>(mv.data()), (size_t)nnz);
+    P->nnz = nnz;
+    P->st.csr_nnz = nnz;
+    int64_t own = mp[P->pt_e] - mp[P->pt_b];
+    P->st.bytes_csr = 20.0 * (double)own + 48.0 * (double)(P->pt_e - P->pt_b);
+    P->st.device_bytes = P->bytes;
+  } catch (const CudaFail& f) {
+    P->sticky_error = true;
+    return f.s;
+  } catch (const std::bad_alloc&) {
+    return FDA_ERR_OOM;
+  }
+  return FDA_OK;
+}
+
+static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, double* out, float* phase_ms) {
+  if (!P || !phi || !out) return FDA_ERR_INVALID_ARG;
+  if (P->host_only) return FDA_ERR_STATE;
+  if (P->sticky_error) return FDA_ERR_CUDA;
+  if ((const void*)phi == (const void*)out) return FDA_ERR_ALIAS;
+  const int64_t n = P->n;
+  cudaStream_t st = P->stream;
+  const bool dphi = is_device_ptr(phi), dout = is_device_ptr(out);
+  if (phase_ms && (!dphi || !dout)) return FDA_ERR_INVALID_ARG;
+  try {
+    const double2* d_phi = reinterpret_cast<const double2*>(phi);
+    double2* d_out = reinterpret_cast<double2*>(out);
+    if (!dphi) {
+      ck(cudaMemcpyAsync(P->phi_buf, phi, (size_t)n * sizeof(double2), cudaMemcpyHostToDevice, st));
+      d_phi = P->phi_buf;
+    }
+    if (!dout) d_out = P->out_buf;
+    cudaEvent_t ev[10];
+    if (phase_ms)
+      for (int i = 0; i < 10; ++i) ck(cudaEventCreate(&ev[i]));
+    auto mark = [&](int i) {
+      if (phase_ms) ck(cudaEventRecord(ev[i], st));
+    };
+    fda::Points Pt{P->px, P->py, P->pz, P->nx, P->ny, P->nz, P->w};
+    fda::LeafGeom Lg{P->leaf_ptr, P->lcx, P->lcy, P->lcz};
+    const double k = P->H.k;
+    const double2 alpha = make_double2(P->H.alpha.real(), P->H.alpha.imag());
+    mark(0);
+    fda::launch_permute_scale(n, P->perm, P->w, d_phi, P->q, P->phim, st);
+    mark(1);
+    const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
+    if (!(mask & FDA_PHASE_NEAR) || partial) ck(cudaMemsetAsync(P->outm, 0, (size_t)n * sizeof(double2), st));
+    if (mask & FDA_PHASE_NEAR)
+      fda::launch_p2p(P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, Pt, P->q, k, alpha, P->outm,
+                      P->leaf_b, st);
+    mark(2);
+    if ((mask & FDA_PHASE_CORR) && P->nnz > 0)
+      fda::launch_csr(P->pt_b, P->pt_e, P->c_ptr, P->c_col, P->c_val, P->phim, P->outm, st);
+    mark(3);
+    const bool far = (mask & FDA_PHASE_FAR) && P->H.lmin >= 0;
+    if (far) {
+      for (const auto& O : P->lo)
+        fda::launch_s2m(O.nleaves, O.leaf, O.slot, Lg, Pt, P->q, O.surf, O.nsurf, O.S, O.s, k, P->lv[O.level].X, st);
+    }
+    mark(4);
+    if (far) {
+      for (int t = (int)P->tr.size() - 1; t >= 0; --t) {
+        const DevTrans& T = P->tr[t];
+        fda::launch_m2m(T.n_par, T.up_ptr, T.up_child, T.up_mat, T.pool, T.sp, T.sc, P->lv[T.lp + 1].X,
+                        P->lv[T.lp].X, st);
+      }
+    }
+    mark(5);
+    if (far) {
+      for (auto& D : P->lv)
+        if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
+      for (auto& D : P->lv)
+        if (D.ngroups)
+          fda::launch_m2l(D.ngroups, D.gbeg, D.gend, D.grank, D.gmat, P->m2l_tgt, P->m2l_src, D.pool, D.s, D.X, D.Y,
+                          st);
+    }
+    mark(6);
+    if (far) {
+      for (const auto& T : P->tr)
+        fda::launch_l2l(T.n_child, T.dn_ptr, T.dn_parent, T.dn_mat, T.poolT, T.sp, T.sc, P->lv[T.lp].Y,
+                        P->lv[T.lp + 1].Y, st);
+    }
+    mark(7);
+    if (far) {
+      for (const auto& O : P->lo)
+        fda::launch_l2t(O.nleaves_own, O.leaf_own, O.slot_own, Lg, Pt, O.surf, O.nsurf, O.T, O.s, k, alpha,
+                        P->lv[O.level].Y, P->outm, st);
+    }
+    mark(8);
+    fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
+    mark(9);
+    ck(cudaGetLastError());
+    if (!dout) {
+      ck(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(double2), cudaMemcpyDeviceToHost, st));
+      ck(cudaStreamSynchronize(st));
+    }
+    if (phase_ms) {
+      ck(cudaEventSynchronize(ev[9]));
+      for (int i = 0; i < 9; ++i) ck(cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]));
+      for (int i = 0; i < 10; ++i) cudaEventDestroy(ev[i]);
+    }
+  } catch (const CudaFail& f) {
+    P->sticky_error = true;
+    return f.s;
+  }
+  return FDA_OK;
+}
+
+fda_status fda_apply(fda_plan P, const double* phi, double* out) { return apply_impl(P, FDA_PHASE_ALL, phi, out, nullptr); }
+fda_status fda_apply_phases(fda_plan P, uint32_t mask, const double* phi, double* out) {
+  return apply_impl(P, mask, phi, out, nullptr);
+}
+fda_status fda_apply_timed(fda_plan P, uint32_t mask, const double* phi, double* out, float* phase_ms) {
+  if (!phase_ms) return FDA_ERR_INVALID_ARG;
+  return apply_impl(P, mask, phi, out, phase_ms);
+}
+
+fda_status fda_plan_stats(fda_plan P, fda_stats* s) {
+  if (!P || !s) return FDA_ERR_INVALID_ARG;
+  *s = P->st;
+  return FDA_OK;
+}
+
+const char* fda_plan_log(fda_plan P) { return P ? P->logstr.c_str() : ""; }
+
+fda_status fda_plan_export_leaves(fda_plan P, int64_t* nleaves, int32_t* leaf_of_point, int32_t* leaf_level,
+                                  int64_t* leaf_ijk) {
+  if (!P || !nleaves) return FDA_ERR_INVALID_ARG;
+  const fda::HostPlan& H = P->H;
+  *nleaves = (int64_t)H.leaves.size();
+  for (size_t t = 0; t < H.leaves.size(); ++t) {
+    const fda::Cube& c = H.cubes[H.leaves[t]];
+    if (leaf_of_point)
+      for (int64_t m = c.pbeg; m < c.pend; ++m) leaf_of_point[H.perm[m]] = (int32_t)t;
+    if (leaf_level) leaf_level[t] = c.level;
+    if (leaf_ijk)
+      for (int d = 0; d < 3; ++d) leaf_ijk[3 * t + d] = c.ijk[d];
+  }
+  return FDA_OK;
+}
+
+fda_status fda_plan_export_p2p(fda_plan P, int64_t* npairs, int32_t* tgt, int32_t* src) {
+  if (!P || !npairs) return FDA_ERR_INVALID_ARG;
+  const fda::HostPlan& H = P->H;
+  *npairs = (int64_t)H.p2p_src.size();
+  if (tgt && src) {
+    for (size_t t = 0; t + 1 < H.p2p_ptr.size(); ++t)
+      for (int64_t e = H.p2p_ptr[t]; e < H.p2p_ptr[t + 1]; ++e) tgt[e] = (int32_t)t, src[e] = (int32_t)H.p2p_src[e];
+  }
+  return FDA_OK;
+}
+
+fda_status fda_plan_export_m2l(fda_plan P, int64_t* npairs, int32_t* level, int64_t* tgt_ijk, int64_t* src_ijk) {
+  if (!P || !npairs) return FDA_ERR_INVALID_ARG;
+  const fda::HostPlan& H = P->H;
+  *npairs = (int64_t)H.m2l_tgt.size();
+  if (level && tgt_ijk && src_ijk) {
+    for (const auto& G : H.m2l_groups) {
+      const fda::Level& L = H.levels[G.level];
+      for (int64_t p = G.pbeg; p < G.pend; ++p) {
+        const fda::Cube& B = H.cubes[L.cubes[L.in_cube[H.m2l_tgt[p]]]];
+        const fda::Cube& C = H.cubes[L.cubes[L.out_cube[H.m2l_src[p]]]];
+        level[p] = G.level;
+        for (int d = 0; d < 3; ++d) tgt_ijk[3 * p + d] = B.ijk[d], src_ijk[3 * p + d] = C.ijk[d];
+      }
+    }
+  }
+  return FDA_OK;
+}
+
+fda_status fda_plan_destroy(fda_plan P) {
+  if (!P) return FDA_ERR_INVALID_ARG;
+  free_plan(P);
+  delete P;
+  return FDA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// kernels.cuh -- device kernels of the FDA Burton-Miller apply (sm_100a, FP64).
+//
+// Notation:
+//   H1 permute+weight   H2 P2P near   H3 correction SpMV   H4 S2M (dipole E_up)
+//   H5 M2M   H6 M2L (dense / low-rank)   H7 L2L (= M2M^T)   H8 L2T (E_dn = G + alpha dG/dn_x)
+//   H9 unpermute
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fda {
+
+struct LeafGeom {        // leaves in Morton order; leaf t owns points [ptr[t], ptr[t+1])
+  const int64_t* ptr;
+  const double* cx;      // leaf centres
+  const double* cy;
+  const double* cz;
+};
+
+struct Points {
+  const double *x, *y, *z, *nx, *ny, *nz, *w;
+};
+
+void launch_permute_scale(int64_t n, const int32_t* perm, const double* w, const double2* phi, double2* q,
+                          double2* phim, cudaStream_t st);
+void launch_unpermute(int64_t n, const int32_t* perm, const double2* outm, double2* out, cudaStream_t st);
+void launch_p2p(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
+                Points P, const double2* q, double k, double2 alpha, double2* outm, int64_t tgt_leaf_begin,
+                cudaStream_t st);
+void launch_csr(int64_t row_begin, int64_t row_end, const int64_t* rp, const int32_t* col, const double2* val,
+                const double2* phim, double2* outm, cudaStream_t st);
+void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
+                const double2* q, const double* surf /* nsurf x 3, relative */, int nsurf, const double2* S,
+                int s, double k, double2* X, cudaStream_t st);
+void launch_m2m(int64_t nparent, const int64_t* up_ptr, const int32_t* up_child, const int32_t* up_mat,
+                const double2* pool, int sp, int sc, const double2* Xc, double2* Xp, cudaStream_t st);
+void launch_l2l(int64_t nchild, const int64_t* dn_ptr, const int32_t* dn_parent, const int32_t* dn_mat,
+                const double2* poolT, int sp, int sc, const double2* Yp, double2* Yc, cudaStream_t st);
+void launch_m2l(int64_t ngroups, const int64_t* gbeg, const int64_t* gend, const int32_t* grank,
+                const int64_t* gmat, const int32_t* tgt, const int32_t* src, const double2* pool, int s,
+                const double2* X, double2* Y, cudaStream_t st);
+void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
+                const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha,
+                const double2* Y, double2* outm, cudaStream_t st);
+
+}  // namespace fda

@@ -1,0 +1,835 @@
+// plan.cpp -- host-side plan builder (tree, lists, wedges, operators).  See plan.hpp.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <sstream>
+#include <unordered_map>
+#include <unordered_set>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace fda {
+
+static const double PI = 3.14159265358979323846;
+static const int MAXD = 21;
+
+static double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------ Morton keys
+static inline uint64_t spread3(uint64_t v) {
+  v &= 0x1fffff;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+static inline uint64_t morton(uint64_t i, uint64_t j, uint64_t k) {
+  return (spread3(i) << 2) | (spread3(j) << 1) | spread3(k);
+}
+static inline uint64_t cube_key(int64_t i, int64_t j, int64_t k) {
+  return ((uint64_t)i << 42) | ((uint64_t)j << 21) | (uint64_t)k;
+}
+
+// ------------------------------------------------------------------ kernel (host, for operators)
+static inline cplx Gk(double k, double dx, double dy, double dz) {
+  const double r = std::sqrt(dx * dx + dy * dy + dz * dz);
+  return std::exp(cplx(0.0, k * r)) / (4.0 * PI * r);
+}
+using P3 = std::array<double, 3>;
+static Mat Gmat(double k, const std::vector<P3>& X, const std::vector<P3>& Y, const double* shiftY = nullptr) {
+  Mat M((int64_t)X.size(), (int64_t)Y.size());
+  const double sx = shiftY ? shiftY[0] : 0, sy = shiftY ? shiftY[1] : 0, sz = shiftY ? shiftY[2] : 0;
+  for (size_t j = 0; j < Y.size(); ++j)
+    for (size_t i = 0; i < X.size(); ++i)
+      M((int64_t)i, (int64_t)j) = Gk(k, X[i][0] - Y[j][0] - sx, X[i][1] - Y[j][1] - sy, X[i][2] - Y[j][2] - sz);
+  return M;
+}
+
+// ------------------------------------------------------------------ directions (face grid)
+int face_dir(const double v[3], int m) {
+  int ax = 0;
+  double best = std::fabs(v[0]);
+  for (int i = 1; i < 3; ++i)
+    if (std::fabs(v[i]) > best) best = std::fabs(v[i]), ax = i;  // tie -> lowest axis
+  const int neg = v[ax] < 0 ? 1 : 0;
+  int o0 = ax == 0 ? 1 : 0, o1 = ax == 2 ? 1 : 2;
+  const double u = v[o0] / best, t = v[o1] / best;
+  int a = (int)std::floor((u + 1.0) * 0.5 * m), b = (int)std::floor((t + 1.0) * 0.5 * m);
+  a = std::min(std::max(a, 0), m - 1);
+  b = std::min(std::max(b, 0), m - 1);
+  const int f = 2 * ax + neg;
+  return (f * m + a) * m + b;
+}
+void dir_center(int d, int m, double out[3]) {
+  const int f = d / (m * m), rem = d % (m * m), a = rem / m, b = rem % m;
+  const int ax = f / 2, neg = f % 2;
+  const int o0 = ax == 0 ? 1 : 0, o1 = ax == 2 ? 1 : 2;
+  double v[3];
+  v[ax] = neg ? -1.0 : 1.0;
+  v[o0] = -1.0 + (2.0 * a + 1.0) / m;
+  v[o1] = -1.0 + (2.0 * b + 1.0) / m;
+  const double nn = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  for (int i = 0; i < 3; ++i) out[i] = v[i] / nn;
+}
+int anti_dir(int d, int m) {
+  const int f = d / (m * m), rem = d % (m * m), a = rem / m, b = rem % m;
+  return ((f ^ 1) * m + (m - 1 - a)) * m + (m - 1 - b);
+}
+int child_dir(int d, int mp) {
+  // parent level (finer grid mp) -> child level (grid mp/2): cell (f, a, b) -> (f, a/2, b/2)
+  const int f = d / (mp * mp), rem = d % (mp * mp), a = rem / mp, b = rem % mp;
+  const int mc = mp / 2;
+  return (f * mc + a / 2) * mc + b / 2;
+}
+
+static std::vector<Sym> all_syms() {
+  std::vector<Sym> g;
+  int p[3] = {0, 1, 2};
+  do {
+    for (int s = 0; s < 8; ++s) {
+      Sym e;
+      for (int i = 0; i < 3; ++i) e.perm[i] = p[i], e.sign[i] = (s >> i) & 1 ? -1 : 1;
+      g.push_back(e);
+    }
+  } while (std::next_permutation(p, p + 3));
+  return g;
+}
+static inline P3 apply_sym(const Sym& g, const P3& v) {
+  return {g.sign[0] * v[g.perm[0]], g.sign[1] * v[g.perm[1]], g.sign[2] * v[g.perm[2]]};
+}
+
+// ------------------------------------------------------------------ LF surface grid
+static std::vector<P3> surface_grid(int p, double side) {
+  std::vector<P3> s;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      for (int k = 0; k < p; ++k) {
+        if (i == 0 || j == 0 || k == 0 || i == p - 1 || j == p - 1 || k == p - 1) {
+          const double h = side / (p - 1);
+          s.push_back({-0.5 * side + i * h, -0.5 * side + j * h, -0.5 * side + k * h});
+        }
+      }
+  return s;
+}
+
+// ------------------------------------------------------------------ build
+std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nrm, const double* w, double k,
+                       cplx alpha, double eps, const Options& opt) {
+  std::ostringstream log;
+  double t0 = now();
+  P.n = n;
+  P.k = k;
+  P.alpha = alpha;
+  P.eps = eps;
+  P.opt = opt;
+  P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
+  // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
+  P.np = opt.np > 0 ? opt.np : (int)std::max(30.0, std::round(50.0 * (-std::log10(eps) - 3.0)));
+  const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;
+
+  // ---- P0: bounding cube, Morton sort
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = 0; i < n; ++i)
+    for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], x[3 * i + d]), hi[d] = std::max(hi[d], x[3 * i + d]);
+  double W = 0;
+  for (int d = 0; d < 3; ++d) W = std::max(W, hi[d] - lo[d]);
+  if (W <= 0) W = 1.0;
+  W *= (1.0 + 1e-6);  // root = bounding cube x (1 + 1e-6)   (R13)
+  double ctr[3];
+  for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]), P.root_lo[d] = ctr[d] - 0.5 * W;
+  P.root_w = W;
+  std::vector<uint64_t> key(n);
+  const double scale = (double)(1 << MAXD) / W;
+#pragma omp parallel for
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t c[3];
+    for (int d = 0; d < 3; ++d) {
+      double u = (x[3 * i + d] - P.root_lo[d]) * scale;
+      int64_t v = (int64_t)std::floor(u);
+      v = std::min<int64_t>(std::max<int64_t>(v, 0), (1 << MAXD) - 1);
+      c[d] = (uint64_t)v;
+    }
+    key[i] = morton(c[0], c[1], c[2]);
+  }
+  std::vector<int32_t> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  P.perm = ord;
+  P.px.resize(n), P.py.resize(n), P.pz.resize(n), P.nx.resize(n), P.ny.resize(n), P.nz.resize(n), P.w.resize(n);
+  std::vector<uint64_t> skey(n);
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = ord[t];
+    P.px[t] = x[3 * i], P.py[t] = x[3 * i + 1], P.pz[t] = x[3 * i + 2];
+    P.nx[t] = nrm[3 * i], P.ny[t] = nrm[3 * i + 1], P.nz[t] = nrm[3 * i + 2];
+    P.w[t] = w[i];
+    skey[t] = key[i];
+  }
+  // coincident points -> error
+  for (int64_t t = 1; t < n; ++t) {
+    if (skey[t] == skey[t - 1]) {
+      const double dx = P.px[t] - P.px[t - 1], dy = P.py[t] - P.py[t - 1], dz = P.pz[t] - P.pz[t - 1];
+      if (std::sqrt(dx * dx + dy * dy + dz * dz) < 1e-14 * W) return "COINCIDENT_POINTS";
+    }
+  }
+
+  // ---- P1: adaptive octree
+  auto level_w = [&](int l) { return W / (double)(1LL << l); };
+  auto is_hf = [&](int l) { return k > 0 && level_w(l) >= lambda; };  // HF iff w >= lambda (R13)
+  P.cubes.clear();
+  {
+    Cube r{};
+    r.level = 0;
+    r.ijk[0] = r.ijk[1] = r.ijk[2] = 0;
+    r.pbeg = 0, r.pend = n, r.parent = -1;
+    for (auto& c : r.child) c = -1;
+    r.leaf = true;
+    P.cubes.push_back(r);
+  }
+  std::vector<std::vector<int64_t>> bylevel(1, std::vector<int64_t>{0});
+  for (int l = 0; l < opt.max_depth; ++l) {
+    std::vector<int64_t> next;
+    for (int64_t ci : bylevel[l]) {
+      Cube c = P.cubes[ci];
+      const int64_t cnt = c.pend - c.pbeg;
+      const bool split = !opt.single_leaf && (cnt > P.np || is_hf(l));
+      if (!split) continue;
+      P.cubes[ci].leaf = false;
+      const int shift = 3 * (MAXD - l - 1);
+      int64_t b = c.pbeg;
+      for (int oct = 0; oct < 8; ++oct) {
+        // first point with octant bits > oct
+        int64_t e = std::upper_bound(skey.begin() + b, skey.begin() + c.pend, (uint64_t)oct,
+                                     [&](uint64_t v, uint64_t kk) { return v < ((kk >> shift) & 7); }) -
+                    skey.begin();
+        if (e > b) {
+          Cube ch{};
+          ch.level = l + 1;
+          ch.ijk[0] = 2 * c.ijk[0] + ((oct >> 2) & 1);
+          ch.ijk[1] = 2 * c.ijk[1] + ((oct >> 1) & 1);
+          ch.ijk[2] = 2 * c.ijk[2] + (oct & 1);
+          ch.pbeg = b, ch.pend = e, ch.parent = ci;
+          for (auto& cc : ch.child) cc = -1;
+          ch.leaf = true;
+          const int64_t id = (int64_t)P.cubes.size();
+          P.cubes.push_back(ch);
+          P.cubes[ci].child[oct] = id;
+          next.push_back(id);
+        }
+        b = e;
+      }
+    }
+    if (next.empty()) break;
+    bylevel.push_back(std::move(next));
+  }
+  const int nlev = (int)bylevel.size();
+  P.levels.assign(nlev, Level());
+  std::vector<std::unordered_map<uint64_t, int64_t>> hmap(nlev);
+  for (int l = 0; l < nlev; ++l) {
+    Level& L = P.levels[l];
+    L.l = l;
+    L.w = level_w(l);
+    L.hf = is_hf(l);
+    L.R = L.hf ? (int)std::floor(1.0 + k * L.w / PI) : 1;  // dist <= c_d k w^2, c_d = 1/pi
+    L.cubes = bylevel[l];
+    hmap[l].reserve(L.cubes.size() * 2);
+    for (size_t t = 0; t < L.cubes.size(); ++t) {
+      Cube& c = P.cubes[L.cubes[t]];
+      c.local = (int64_t)t;
+      hmap[l][cube_key(c.ijk[0], c.ijk[1], c.ijk[2])] = L.cubes[t];
+    }
+  }
+  // HF direction grids: m_L = ceil(k w_L / pi) at the finest HF level, doubling upwards (R15)
+  int Lhf = -1;
+  for (int l = 0; l < nlev; ++l)
+    if (P.levels[l].hf) Lhf = l;
+  if (Lhf >= 0) {
+    const int mL = std::max(1, (int)std::ceil(k * P.levels[Lhf].w / PI - 1e-12));
+    for (int l = Lhf; l >= 0; --l) {
+      Level& L = P.levels[l];
+      const int64_t mm = (int64_t)mL << (Lhf - l);
+      L.m = (int)std::min<int64_t>(mm, 1 << 12);
+      L.ndir = 6 * L.m * L.m;
+    }
+  }
+  for (int64_t ci = 0; ci < (int64_t)P.cubes.size(); ++ci)
+    if (P.cubes[ci].leaf) P.leaves.push_back(ci);
+  std::sort(P.leaves.begin(), P.leaves.end(),
+            [&](int64_t a, int64_t b) { return P.cubes[a].pbeg < P.cubes[b].pbeg; });
+  P.leaf_of_cube.assign(P.cubes.size(), -1);
+  for (size_t t = 0; t < P.leaves.size(); ++t) P.leaf_of_cube[P.leaves[t]] = (int64_t)t;
+  P.t_tree = now() - t0;
+  t0 = now();
+
+  auto find = [&](int l, int64_t i, int64_t j, int64_t kk) -> int64_t {
+    const int64_t lim = 1LL << l;
+    if (i < 0 || j < 0 || kk < 0 || i >= lim || j >= lim || kk >= lim) return -1;
+    auto it = hmap[l].find(cube_key(i, j, kk));
+    return it == hmap[l].end() ? -1 : it->second;
+  };
+
+  // ---- P2: P2P lists.  Leaf pair (T, S) is direct iff their ancestors at min(lev T, lev S)
+  // are adjacent (R20); everything else is covered by exactly one M2L.
+  {
+    const int64_t nl = (int64_t)P.leaves.size();
+    std::vector<std::vector<int64_t>> src(nl);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < nl; ++t) {
+      const Cube& T = P.cubes[P.leaves[t]];
+      std::vector<int64_t>& out = src[t];
+      std::vector<int64_t> stack;
+      for (int dx = -1; dx <= 1; ++dx)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dz = -1; dz <= 1; ++dz) {
+            int64_t a = find(T.level, T.ijk[0] + dx, T.ijk[1] + dy, T.ijk[2] + dz);
+            if (a < 0) continue;
+            stack.push_back(a);
+            while (!stack.empty()) {
+              int64_t c = stack.back();
+              stack.pop_back();
+              if (P.cubes[c].leaf) {
+                out.push_back(P.leaf_of_cube[c]);
+                continue;
+              }
+              for (int o = 0; o < 8; ++o)
+                if (P.cubes[c].child[o] >= 0) stack.push_back(P.cubes[c].child[o]);
+            }
+          }
+      int64_t anc = T.parent;
+      while (anc >= 0) {
+        const Cube& A = P.cubes[anc];
+        for (int dx = -1; dx <= 1; ++dx)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dz = -1; dz <= 1; ++dz) {
+              if (!dx && !dy && !dz) continue;
+              int64_t a = find(A.level, A.ijk[0] + dx, A.ijk[1] + dy, A.ijk[2] + dz);
+              if (a >= 0 && P.cubes[a].leaf) out.push_back(P.leaf_of_cube[a]);
+            }
+        anc = A.parent;
+      }
+      std::sort(out.begin(), out.end());
+    }
+    P.p2p_ptr.assign(nl + 1, 0);
+    for (int64_t t = 0; t < nl; ++t) P.p2p_ptr[t + 1] = P.p2p_ptr[t] + (int64_t)src[t].size();
+    P.p2p_src.resize(P.p2p_ptr[nl]);
+    for (int64_t t = 0; t < nl; ++t) std::copy(src[t].begin(), src[t].end(), P.p2p_src.begin() + P.p2p_ptr[t]);
+  }
+
+  // ---- P2: interaction lists per level, grouped by offset (counting sort)
+  struct PairL {
+    int32_t b, c;
+  };
+  std::vector<std::vector<int32_t>> lv_off_key(nlev);   // per level: offset keys present
+  std::vector<std::vector<std::vector<PairL>>> lv_pairs(nlev);  // per level per offset-key-index
+  std::vector<std::vector<std::array<int, 3>>> lv_offs(nlev);
+  for (int l = 1; l < nlev; ++l) {
+    const Level& L = P.levels[l];
+    const Level& Lp = P.levels[l - 1];
+    const int Rp = Lp.R, Rc = L.R;
+    const int span = 2 * Rp + 1;          // children offsets |delta| <= 2 Rp + 1
+    const int D = 2 * span + 1;
+    std::vector<std::vector<PairL>> buckets((size_t)D * D * D);
+    const int64_t npar = (int64_t)Lp.cubes.size();
+    const bool brute = (int64_t)(2 * Rp + 1) * (2 * Rp + 1) * (2 * Rp + 1) > npar;
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    std::vector<std::vector<std::vector<PairL>>> tb(nth, std::vector<std::vector<PairL>>());
+#pragma omp parallel
+    {
+      int tid = 0;
+#ifdef _OPENMP
+      tid = omp_get_thread_num();
+#endif
+      auto& mine = tb[tid];
+      mine.assign((size_t)D * D * D, {});
+      std::vector<int64_t> nearp;
+#pragma omp for schedule(dynamic, 4)
+      for (int64_t pi = 0; pi < npar; ++pi) {
+        const Cube& Pc = P.cubes[Lp.cubes[pi]];
+        if (Pc.leaf) continue;
+        nearp.clear();
+        if (brute) {
+          for (int64_t q = 0; q < npar; ++q) {
+            const Cube& Q = P.cubes[Lp.cubes[q]];
+            int64_t dm = 0;
+            for (int d = 0; d < 3; ++d) dm = std::max<int64_t>(dm, std::llabs(Q.ijk[d] - Pc.ijk[d]));
+            if (dm <= Rp) nearp.push_back(Lp.cubes[q]);
+          }
+        } else {
+          for (int dx = -Rp; dx <= Rp; ++dx)
+            for (int dy = -Rp; dy <= Rp; ++dy)
+              for (int dz = -Rp; dz <= Rp; ++dz) {
+                int64_t a = find(l - 1, Pc.ijk[0] + dx, Pc.ijk[1] + dy, Pc.ijk[2] + dz);
+                if (a >= 0) nearp.push_back(a);
+              }
+        }
+        for (int ob = 0; ob < 8; ++ob) {
+          const int64_t bi = Pc.child[ob];
+          if (bi < 0) continue;
+          const Cube& B = P.cubes[bi];
+          for (int64_t qa : nearp) {
+            const Cube& Q = P.cubes[qa];
+            for (int oc = 0; oc < 8; ++oc) {
+              const int64_t cidx = Q.child[oc];
+              if (cidx < 0) continue;
+              const Cube& C = P.cubes[cidx];
+              int dl[3];
+              int dm = 0;
+              for (int d = 0; d < 3; ++d) dl[d] = (int)(B.ijk[d] - C.ijk[d]), dm = std::max(dm, std::abs(dl[d]));
+              if (dm <= Rc) continue;  // near at this level
+              const size_t key = ((size_t)(dl[0] + span) * D + (dl[1] + span)) * D + (dl[2] + span);
+              mine[key].push_back({(int32_t)B.local, (int32_t)C.local});
+            }
+          }
+        }
+      }
+    }
+    std::vector<int32_t> keys;
+    for (size_t key = 0; key < buckets.size(); ++key) {
+      size_t tot = 0;
+      for (int t = 0; t < nth; ++t) tot += tb[t][key].size();
+      if (!tot) continue;
+      std::vector<PairL> v;
+      v.reserve(tot);
+      for (int t = 0; t < nth; ++t) v.insert(v.end(), tb[t][key].begin(), tb[t][key].end());
+      std::sort(v.begin(), v.end(), [](const PairL& a, const PairL& b) { return a.b < b.b; });
+      lv_pairs[l].push_back(std::move(v));
+      const int kk = (int)key;
+      lv_offs[l].push_back({kk / (D * D) - span, (kk / D) % D - span, kk % D - span});
+    }
+    if (!lv_pairs[l].empty() && P.lmin < 0) P.lmin = l;
+  }
+  P.t_lists = now() - t0;
+  t0 = now();
+
+  // ---- slots
+  const int lmin = P.lmin;
+  std::vector<std::vector<int>> grp_dir(nlev);
+  for (int l = 0; l < nlev; ++l) {
+    Level& L = P.levels[l];
+    const int64_t nc = (int64_t)L.cubes.size();
+    L.out_slot.assign(nc * L.ndir, -1);
+    L.in_slot.assign(nc * L.ndir, -1);
+    grp_dir[l].assign(lv_offs[l].size(), 0);
+    if (lmin < 0 || l < lmin) continue;
+    auto add_out = [&](int64_t c, int d) {
+      int64_t& s = L.out_slot[c * L.ndir + d];
+      if (s < 0) s = 1;
+    };
+    auto add_in = [&](int64_t c, int d) {
+      int64_t& s = L.in_slot[c * L.ndir + d];
+      if (s < 0) s = 1;
+    };
+    if (!L.hf) {
+      for (int64_t c = 0; c < nc; ++c) add_out(c, 0), add_in(c, 0);
+    } else {
+      for (size_t g = 0; g < lv_offs[l].size(); ++g) {
+        const double v[3] = {(double)lv_offs[l][g][0], (double)lv_offs[l][g][1], (double)lv_offs[l][g][2]};
+        const int d = face_dir(v, L.m);  // source -> target direction
+        grp_dir[l][g] = d;
+        const int t = anti_dir(d, L.m);
+        for (const PairL& pr : lv_pairs[l][g]) add_out(pr.c, d), add_in(pr.b, t);
+      }
+      if (l - 1 >= lmin && P.levels[l - 1].hf) {  // closure from parent slots
+        const Level& Lp = P.levels[l - 1];
+        for (int64_t pc = 0; pc < (int64_t)Lp.cubes.size(); ++pc) {
+          const Cube& Pc = P.cubes[Lp.cubes[pc]];
+          for (int d = 0; d < Lp.ndir; ++d) {
+            const bool o = Lp.out_slot[pc * Lp.ndir + d] >= 0, i = Lp.in_slot[pc * Lp.ndir + d] >= 0;
+            if (!o && !i) continue;
+            const int cd = child_dir(d, Lp.m);
+            for (int oc = 0; oc < 8; ++oc) {
+              if (Pc.child[oc] < 0) continue;
+              const int64_t cl = P.cubes[Pc.child[oc]].local;
+              if (o) add_out(cl, cd);
+              if (i) add_in(cl, cd);
+            }
+          }
+        }
+      }
+    }
+    // number the slots (cube-major, so a cube's directions are contiguous)
+    for (int64_t c = 0; c < nc; ++c)
+      for (int d = 0; d < L.ndir; ++d) {
+        int64_t& so = L.out_slot[c * L.ndir + d];
+        if (so >= 0) {
+          so = L.n_out++;
+          L.out_cube.push_back(c);
+          L.out_dir.push_back(d);
+        }
+        int64_t& si = L.in_slot[c * L.ndir + d];
+        if (si >= 0) {
+          si = L.n_in++;
+          L.in_cube.push_back(c);
+          L.in_dir.push_back(d);
+        }
+      }
+  }
+
+  // ---- P3: operators.  LF surfaces.
+  const double eps_int = P.eps_int;
+  for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
+    Level& L = P.levels[l];
+    if (L.hf || L.n_out == 0) continue;
+    const double wl = k > 0 ? L.w / lambda : 0.0;
+    L.p = wl < opt.lf_p_switch ? opt.lf_p_low : opt.lf_p_high;
+    L.eq_pts = surface_grid(L.p, 1.05 * L.w);  // outgoing equivalent = incoming check (inner)
+    L.ck_pts = surface_grid(L.p, 2.95 * L.w);  // outgoing check = incoming equivalent (outer)
+    L.nsurf = (int)L.eq_pts.size();
+    Mat R = Gmat(k, L.ck_pts, L.eq_pts);      // [R_up]_ij = G(a_i, b_j)
+    SVD sv = svd_truncated(R, eps_int);       // eq_svdr / eq_invr
+    L.lfU = sv.U;
+    L.lfV = sv.V;
+    L.lfsig = sv.s;
+    L.s = (int)sv.s.size();
+  }
+
+  // ---- P3: HF directional sets, top-down (R16)
+  const std::vector<Sym> syms = all_syms();
+  for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
+    Level& L = P.levels[l];
+    if (!L.hf || (L.n_out == 0 && L.n_in == 0)) continue;
+    const int m = L.m, nd = L.ndir;
+    L.dir_rep.assign(nd, -1);
+    L.dir_sym.assign(nd, Sym());
+    std::vector<char> used(nd, 0);
+    for (int64_t s = 0; s < L.n_out; ++s) used[L.out_dir[s]] = 1;
+    for (int64_t s = 0; s < L.n_in; ++s) used[L.in_dir[s]] = 1;
+    // orbit representatives
+    std::vector<int> rep_of(nd, -1);
+    std::vector<int> repdirs;
+    for (int d = 0; d < nd; ++d) {
+      double c[3];
+      dir_center(d, m, c);
+      int best = d;
+      for (const Sym& g : syms) {
+        P3 v = apply_sym(g, {c[0], c[1], c[2]});
+        best = std::min(best, face_dir(v.data(), m));
+      }
+      rep_of[d] = best;
+    }
+    std::vector<char> rep_used(nd, 0);
+    for (int d = 0; d < nd; ++d)
+      if (used[d]) rep_used[rep_of[d]] = 1;
+    std::vector<int> rep_index(nd, -1);
+    for (int d = 0; d < nd; ++d)
+      if (rep_used[d]) rep_index[d] = (int)repdirs.size(), repdirs.push_back(d);
+    for (int d = 0; d < nd; ++d) {
+      if (!rep_used[rep_of[d]]) continue;
+      double c[3];
+      dir_center(rep_of[d], m, c);
+      for (const Sym& g : syms) {
+        P3 v = apply_sym(g, {c[0], c[1], c[2]});
+        if (face_dir(v.data(), m) == d) {
+          L.dir_sym[d] = g;
+          break;
+        }
+      }
+      L.dir_rep[d] = rep_index[rep_of[d]];
+    }
+    L.reps.assign(repdirs.size(), DirRep());
+    // candidate equivalent points: two box-surface layers (1.05 W and 0.7 W)
+    const double sp = opt.hf_spacing * lambda;
+    const int ng = std::max(4, (int)std::ceil(1.05 * L.w / sp) + 1);
+    const int ng2 = std::max(3, (int)std::ceil(0.7 * L.w / sp) + 1);
+    std::vector<P3> cand = surface_grid(ng, 1.05 * L.w);
+    {
+      std::vector<P3> c2 = surface_grid(ng2, 0.7 * L.w);
+      cand.insert(cand.end(), c2.begin(), c2.end());
+    }
+    const std::vector<P3> tbox = [&] {
+      std::vector<P3> t = surface_grid(3, 1.05 * L.w);
+      t.push_back({0, 0, 0});
+      return t;
+    }();
+    const int Rp = P.levels[l - 1].R;
+    const int span = 2 * Rp + 1;
+    const bool parent_slots = (l - 1 >= lmin) && P.levels[l - 1].hf && !P.levels[l - 1].reps.empty();
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int ri = 0; ri < (int)repdirs.size(); ++ri) {
+      const int rd = repdirs[ri];
+      std::vector<P3> rows;
+      // (a) target boxes of every class offset in this wedge
+      for (int i = -span; i <= span; ++i)
+        for (int j = -span; j <= span; ++j)
+          for (int kk = -span; kk <= span; ++kk) {
+            const int dm = std::max({std::abs(i), std::abs(j), std::abs(kk)});
+            if (dm <= L.R) continue;
+            const double v[3] = {(double)i, (double)j, (double)kk};
+            if (face_dir(v, m) != rd) continue;
+            for (const P3& t : tbox) rows.push_back({i * L.w + t[0], j * L.w + t[1], kk * L.w + t[2]});
+          }
+      // (b) parent check points of the nested parent directions, seen from each child position
+      if (parent_slots) {
+        const Level& Lp = P.levels[l - 1];
+        for (int pd = 0; pd < Lp.ndir; ++pd) {
+          if (child_dir(pd, Lp.m) != rd || Lp.dir_rep[pd] < 0) continue;
+          const DirRep& pr = Lp.reps[Lp.dir_rep[pd]];
+          for (const P3& a0 : pr.ap) {
+            const P3 a = apply_sym(Lp.dir_sym[pd], a0);
+            for (int oc = 0; oc < 8; ++oc) {
+              const double o[3] = {(((oc >> 2) & 1) ? 0.5 : -0.5) * L.w, (((oc >> 1) & 1) ? 0.5 : -0.5) * L.w,
+                                   ((oc & 1) ? 0.5 : -0.5) * L.w};
+              rows.push_back({a[0] - o[0], a[1] - o[1], a[2] - o[2]});
+            }
+          }
+        }
+      }
+      if ((int)rows.size() > opt.hf_max_rows) {
+        std::mt19937_64 rng(1234567u + 7919u * (uint64_t)rd + 104729u * (uint64_t)l);
+        std::shuffle(rows.begin(), rows.end(), rng);
+        rows.resize(opt.hf_max_rows);
+      }
+      Mat A = Gmat(k, rows, cand);
+      for (int64_t i = 0; i < A.m; ++i) {
+        const double rr = std::sqrt(rows[i][0] * rows[i][0] + rows[i][1] * rows[i][1] + rows[i][2] * rows[i][2]);
+        for (int64_t j = 0; j < A.n; ++j) A(i, j) *= rr;
+      }
+      std::vector<int64_t> J = pivoted_qr(A, eps_int, 2000);
+      Mat AJt((int64_t)J.size(), A.m);
+      for (int64_t i = 0; i < A.m; ++i)
+        for (size_t t = 0; t < J.size(); ++t) AJt((int64_t)t, i) = A(i, J[t]);
+      std::vector<int64_t> I = pivoted_qr(AJt, eps_int, 2000);
+      DirRep& D = L.reps[ri];
+      D.dir = rd;
+      for (int64_t j : J) D.bp.push_back(cand[j]);
+      for (int64_t i : I) D.ap.push_back(rows[i]);
+      Mat R = Gmat(k, D.ap, D.bp);
+      SVD sv = svd_truncated(R, eps_int);
+      D.U = sv.U;
+      D.V = sv.V;
+      D.sig = sv.s;
+    }
+    int smax = 0;
+    for (auto& D : L.reps) smax = std::max(smax, (int)D.sig.size());
+    L.s = smax;
+    if (opt.verbose) {
+      log << "level " << l << " HF m=" << m << " reps=" << L.reps.size() << " s=" << smax << " ranks:";
+      for (auto& D : L.reps) log << " " << D.bp.size() << "/" << D.sig.size();
+      log << "\n";
+    }
+  }
+
+  // point sets of a slot direction (relative to the cube centre)
+  auto hf_b = [&](const Level& L, int d) {
+    const DirRep& D = L.reps[L.dir_rep[d]];
+    std::vector<P3> v;
+    for (const P3& p : D.bp) v.push_back(apply_sym(L.dir_sym[d], p));
+    return v;
+  };
+  auto hf_a = [&](const Level& L, int d) {
+    const DirRep& D = L.reps[L.dir_rep[d]];
+    std::vector<P3> v;
+    for (const P3& p : D.ap) v.push_back(apply_sym(L.dir_sym[d], p));
+    return v;
+  };
+  // Vt/U factors of a slot direction
+  auto lvV = [&](const Level& L, int d) -> const Mat& { return L.hf ? L.reps[L.dir_rep[d]].V : L.lfV; };
+  auto lvU = [&](const Level& L, int d) -> const Mat& { return L.hf ? L.reps[L.dir_rep[d]].U : L.lfU; };
+  auto lvS = [&](const Level& L, int d) -> const std::vector<double>& {
+    return L.hf ? L.reps[L.dir_rep[d]].sig : L.lfsig;
+  };
+  auto lv_eq = [&](const Level& L, int d) { return L.hf ? hf_b(L, d) : L.eq_pts; };
+  auto lv_ck = [&](const Level& L, int d) { return L.hf ? hf_a(L, d) : L.ck_pts; };
+
+  // ---- M2M / L2L matrices per transition (PAPER.md eq_cmpm / eq_cmpl: L~ = M~^T)
+  for (int lp = std::max(lmin, 0); lmin >= 0 && lp + 1 < nlev; ++lp) {
+    Level& Lp = P.levels[lp];
+    Level& Lc = P.levels[lp + 1];
+    if ((Lp.n_out == 0 && Lp.n_in == 0) || (Lc.n_out == 0 && Lc.n_in == 0)) continue;
+    HostPlan::Trans T;
+    T.lp = lp;
+    T.sp = Lp.s;
+    T.sc = Lc.s;
+    T.mat_index.assign((size_t)Lp.ndir * 8, -1);
+    std::vector<std::pair<int, int>> need;  // (dir, oct)
+    std::vector<char> mark((size_t)Lp.ndir * 8, 0);
+    auto cdir = [&](int d) { return Lc.hf ? child_dir(d, Lp.m) : 0; };
+    // M2M: parent out slots
+    T.up_ptr.assign(Lp.n_out + 1, 0);
+    for (int64_t s = 0; s < Lp.n_out; ++s) {
+      const Cube& Pc = P.cubes[Lp.cubes[Lp.out_cube[s]]];
+      const int d = Lp.out_dir[s];
+      for (int oc = 0; oc < 8; ++oc) {
+        if (Pc.child[oc] < 0) continue;
+        const int64_t cl = P.cubes[Pc.child[oc]].local;
+        const int64_t cs = Lc.out_slot[cl * Lc.ndir + cdir(d)];
+        if (cs < 0) continue;
+        T.up_child.push_back(cs);
+        T.up_mat.push_back(d * 8 + oc);
+        if (!mark[d * 8 + oc]) mark[d * 8 + oc] = 1, need.push_back({d, oc});
+      }
+      T.up_ptr[s + 1] = (int64_t)T.up_child.size();
+    }
+    // L2L: child in slots <- parent in slots
+    T.dn_ptr.assign(Lc.n_in + 1, 0);
+    for (int64_t s = 0; s < Lc.n_in; ++s) {
+      const Cube& C = P.cubes[Lc.cubes[Lc.in_cube[s]]];
+      const Cube& Pc = P.cubes[C.parent];
+      int oc = -1;
+      for (int o = 0; o < 8; ++o)
+        if (Pc.child[o] >= 0 && P.cubes[Pc.child[o]].local == C.local && P.cubes[Pc.child[o]].level == C.level) oc = o;
+      const int dc = Lc.in_dir[s];
+      for (int d = 0; d < Lp.ndir; ++d) {
+        if (cdir(d) != dc) continue;
+        const int64_t ps = Lp.in_slot[Pc.local * Lp.ndir + d];
+        if (ps < 0) continue;
+        T.dn_parent.push_back(ps);
+        T.dn_mat.push_back(d * 8 + oc);
+        if (!mark[d * 8 + oc]) mark[d * 8 + oc] = 1, need.push_back({d, oc});
+      }
+      T.dn_ptr[s + 1] = (int64_t)T.dn_parent.size();
+    }
+    const int64_t msz = (int64_t)T.sp * T.sc;
+    T.pool.assign(need.size() * msz, cplx(0));
+    T.poolT.assign(need.size() * msz, cplx(0));
+    for (size_t t = 0; t < need.size(); ++t) T.mat_index[need[t].first * 8 + need[t].second] = (int64_t)t;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t t = 0; t < (int64_t)need.size(); ++t) {
+      const int d = need[t].first, oc = need[t].second;
+      const double o[3] = {(((oc >> 2) & 1) ? 0.5 : -0.5) * Lc.w, (((oc >> 1) & 1) ? 0.5 : -0.5) * Lc.w,
+                           ((oc & 1) ? 0.5 : -0.5) * Lc.w};
+      const int dc = cdir(d);
+      std::vector<P3> aP = lv_ck(Lp, d);
+      std::vector<P3> bC = lv_eq(Lc, dc);
+      for (auto& p : bC) p = {p[0] + o[0], p[1] + o[1], p[2] + o[2]};
+      Mat E = Gmat(k, aP, bC);                           // E_up: parent check <- child equivalent
+      Mat UhE = gemm(lvU(Lp, d), 'C', E, 'N');           // U^H E
+      Mat M = gemm(UhE, 'N', lvV(Lc, dc), 'N');          // U^H E V_child
+      const std::vector<double>& sg = lvS(Lp, d);
+      cplx* dst = T.pool.data() + t * msz;
+      cplx* dstT = T.poolT.data() + t * msz;
+      for (int64_t j = 0; j < M.n; ++j)
+        for (int64_t i = 0; i < M.m; ++i) {
+          const cplx v = M(i, j) / sg[i];                // Sigma^-1 U^H E_up V~   (eq_cmpm)
+          dst[i + j * T.sp] = v;
+          dstT[j + i * T.sc] = v;
+        }
+    }
+    P.trans.push_back(std::move(T));
+  }
+
+  // ---- M2L groups: K~ = U_dn^H K V_up = V^T G(delta + b_tgt, b_src) V   (eq_cmpk), low rank (eq_lrdk)
+  P.m2l_pool.assign(nlev, {});
+  for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
+    Level& L = P.levels[l];
+    const int s = L.s;
+    const int64_t ng = (int64_t)lv_offs[l].size();
+    if (!ng) continue;
+    std::vector<std::vector<cplx>> gm(ng);
+    std::vector<int> grank(ng, -1);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t g = 0; g < ng; ++g) {
+      const int d = L.hf ? grp_dir[l][g] : 0;
+      const int t = L.hf ? anti_dir(d, L.m) : 0;
+      const double sh[3] = {-lv_offs[l][g][0] * L.w, -lv_offs[l][g][1] * L.w, -lv_offs[l][g][2] * L.w};
+      std::vector<P3> bt = lv_eq(L, t), bs = lv_eq(L, d);
+      Mat K = Gmat(k, bt, bs, sh);   // G(delta w + b_t, b_s) with shiftY = -delta w
+      const Mat& Vt = lvV(L, t);
+      const Mat& Vs = lvV(L, d);
+      Mat Kt = gemm(gemm(Vt, 'T', K, 'N'), 'N', Vs, 'N');   // (st x ss)
+      int rank = -1;
+      std::vector<cplx>& out = gm[g];
+      if (opt.lowrank && Kt.m > 1) {
+        Mat Q, Rq;
+        std::vector<int64_t> piv = pivoted_qr(Kt, 0.1 * eps_int, Kt.n, &Q, &Rq);
+        SVD sv = svd_truncated(Rq, 0.0);
+        int r = 0;
+        for (double v : sv.s)
+          if (v >= eps_int * sv.s[0]) ++r;
+        if (2 * r < std::max(Kt.m, Kt.n)) {
+          rank = r;
+          // U^ = Q U_R S (s x r), V^ = V_R^H (r x s), padded to the level size
+          Mat QU = gemm(Q, 'N', sv.U, 'N');
+          out.assign((size_t)2 * s * r, cplx(0));
+          for (int c = 0; c < r; ++c)
+            for (int64_t i = 0; i < QU.m; ++i) out[i + (size_t)c * s] = QU(i, c) * sv.s[c];
+          cplx* vh = out.data() + (size_t)s * r;
+          for (int64_t j = 0; j < sv.V.m; ++j)
+            for (int c = 0; c < r; ++c) vh[c + (size_t)j * r] = std::conj(sv.V(j, c));
+        }
+      }
+      if (rank < 0) {
+        out.assign((size_t)s * s, cplx(0));
+        for (int64_t j = 0; j < Kt.n; ++j)
+          for (int64_t i = 0; i < Kt.m; ++i) out[i + (size_t)j * s] = Kt(i, j);
+      }
+      grank[g] = rank;
+    }
+    std::vector<cplx>& pool = P.m2l_pool[l];
+    for (int64_t g = 0; g < ng; ++g) {
+      HostPlan::M2LGroup G;
+      G.level = l;
+      G.off[0] = lv_offs[l][g][0], G.off[1] = lv_offs[l][g][1], G.off[2] = lv_offs[l][g][2];
+      G.dir = L.hf ? grp_dir[l][g] : 0;
+      G.rank = grank[g];
+      G.mat_off = (int64_t)pool.size();
+      pool.insert(pool.end(), gm[g].begin(), gm[g].end());
+      G.pbeg = (int64_t)P.m2l_tgt.size();
+      const int t = L.hf ? anti_dir(G.dir, L.m) : 0;
+      for (const PairL& pr : lv_pairs[l][g]) {
+        P.m2l_tgt.push_back(L.in_slot[(int64_t)pr.b * L.ndir + t]);
+        P.m2l_src.push_back(L.out_slot[(int64_t)pr.c * L.ndir + G.dir]);
+      }
+      G.pend = (int64_t)P.m2l_tgt.size();
+      P.m2l_groups.push_back(G);
+      std::vector<cplx>().swap(gm[g]);
+    }
+  }
+
+  // ---- S2M / L2T leaf operators per LF level (eq_cmps, eq_cmpt)
+  for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
+    Level& L = P.levels[l];
+    if (L.hf || L.n_out == 0) continue;
+    HostPlan::LeafOps O;
+    O.level = l;
+    for (int64_t c = 0; c < (int64_t)L.cubes.size(); ++c) {
+      const int64_t gid = L.cubes[c];
+      if (!P.cubes[gid].leaf) continue;
+      O.leaf.push_back(P.leaf_of_cube[gid]);
+      O.slot.push_back(L.out_slot[c]);  // LF: out slot == in slot == cube local index
+    }
+    if (O.leaf.empty()) continue;
+    const int s = L.s, ns = L.nsurf;
+    O.S.assign((size_t)s * ns, cplx(0));
+    O.T.assign((size_t)ns * s, cplx(0));
+    for (int r = 0; r < s; ++r)
+      for (int i = 0; i < ns; ++i) {
+        O.S[r + (size_t)i * s] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // Sigma^-1 U^H
+        O.T[i + (size_t)r * ns] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // conj(U) Sigma^-1
+      }
+    P.leafops.push_back(std::move(O));
+  }
+  P.t_ops = now() - t0;
+  if (opt.verbose) {
+    log << "tree " << P.t_tree << "s lists " << P.t_lists << "s ops " << P.t_ops << "s; levels " << nlev
+        << " leaves " << P.leaves.size() << " lmin " << lmin << "\n";
+    for (int l = 0; l < nlev; ++l) {
+      const Level& L = P.levels[l];
+      int64_t npairs = 0, ngrp = 0, nlow = 0;
+      for (auto& G : P.m2l_groups)
+        if (G.level == l) npairs += G.pend - G.pbeg, ++ngrp, nlow += G.rank >= 0;
+      log << "  L" << l << " w/lambda=" << (k > 0 ? L.w / lambda : 0) << (L.hf ? " HF" : " LF") << " R=" << L.R
+          << " m=" << L.m << " cubes=" << L.cubes.size() << " s=" << L.s << " out=" << L.n_out << " in=" << L.n_in
+          << " m2l_pairs=" << npairs << " groups=" << ngrp << " lowrank=" << nlow << "\n";
+    }
+    P.log = log.str();
+  }
+  return "";
+}
+
+}  // namespace fda

@@ -1,0 +1,238 @@
+"""Thin ctypes binding of libfda.so (include/fda.h).  Argument marshalling only.
+
+Every function here has the name of the C entry point it calls.  Arrays may be
+torch tensors (CUDA or CPU) or numpy arrays; they are passed by pointer.  There
+is no Python or CPU implementation of any step: if libfda.so is missing the
+import fails, and without a CUDA device fda_plan_create raises (FDA_ERR_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libfda.so")
+if not os.path.exists(_LIBPATH):
+    raise ImportError(f"{_LIBPATH} not built: run `python -m paper_1311_5202_b200.build` "
+                      "(the CUDA path has no fallback)")
+_lib = ctypes.CDLL(_LIBPATH)
+
+FDA_OK = 0
+STATUS = {0: "FDA_OK", 1: "FDA_ERR_INVALID_ARG", 2: "FDA_ERR_COINCIDENT_POINTS", 3: "FDA_ERR_ALIAS",
+          4: "FDA_ERR_CUDA", 5: "FDA_ERR_OOM", 6: "FDA_ERR_SETUP_ACCURACY", 7: "FDA_ERR_NCCL", 8: "FDA_ERR_STATE"}
+FDA_PHASE_NEAR, FDA_PHASE_CORR, FDA_PHASE_FAR, FDA_PHASE_ALL = 1, 2, 4, 7
+PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute")
+
+# every symbol include/fda.h declares (checked by tests/test_abi.py)
+EXPORTS = ("fda_options_default", "fda_plan_create", "fda_plan_create_ex", "fda_plan_set_correction", "fda_apply",
+           "fda_apply_phases", "fda_apply_timed", "fda_plan_set_stream", "fda_plan_stats", "fda_plan_log",
+           "fda_plan_export_leaves", "fda_plan_export_p2p", "fda_plan_export_m2l", "fda_plan_destroy",
+           "fda_status_str")
+
+
+class fda_options(ctypes.Structure):
+    _fields_ = [("leaf_size", ctypes.c_int32), ("eps_internal", ctypes.c_double), ("lf_p_low", ctypes.c_int32),
+                ("lf_p_high", ctypes.c_int32), ("lf_p_switch", ctypes.c_double), ("lowrank", ctypes.c_int32),
+                ("single_leaf", ctypes.c_int32), ("hf_max_rows", ctypes.c_int32), ("hf_spacing", ctypes.c_double),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("verbose", ctypes.c_int32),
+                ("host_only", ctypes.c_int32)]
+
+
+class fda_stats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in
+                ("n", "nleaves", "nlevels", "lmin", "p2p_leaf_pairs", "p2p_point_pairs", "m2l_pairs", "m2l_groups",
+                 "m2l_lowrank_groups", "out_slots", "in_slots", "csr_nnz", "device_bytes", "owned_begin",
+                 "owned_end")] + \
+               [(f, ctypes.c_double) for f in
+                ("setup_tree_s", "setup_lists_s", "setup_ops_s", "setup_upload_s", "flops_p2p", "flops_m2l",
+                 "flops_m2m", "flops_l2l", "flops_s2m", "flops_l2t", "bytes_csr")]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_lib.fda_options_default.argtypes = [ctypes.POINTER(fda_options)]
+_lib.fda_options_default.restype = None
+_lib.fda_plan_create.argtypes = [_I64, _P, _P, _P, _D, _D, _D, _D, ctypes.POINTER(_P)]
+_lib.fda_plan_create_ex.argtypes = [_I64, _P, _P, _P, _D, _D, _D, _D, ctypes.POINTER(fda_options), ctypes.POINTER(_P)]
+_lib.fda_plan_set_correction.argtypes = [_P, _I64, _P, _P, _P]
+_lib.fda_apply.argtypes = [_P, _P, _P]
+_lib.fda_apply_phases.argtypes = [_P, ctypes.c_uint32, _P, _P]
+_lib.fda_apply_timed.argtypes = [_P, ctypes.c_uint32, _P, _P, ctypes.POINTER(ctypes.c_float)]
+_lib.fda_plan_set_stream.argtypes = [_P, _P]
+_lib.fda_plan_stats.argtypes = [_P, ctypes.POINTER(fda_stats)]
+_lib.fda_plan_log.argtypes = [_P]
+_lib.fda_plan_log.restype = ctypes.c_char_p
+_lib.fda_plan_export_leaves.argtypes = [_P, ctypes.POINTER(_I64), _P, _P, _P]
+_lib.fda_plan_export_p2p.argtypes = [_P, ctypes.POINTER(_I64), _P, _P]
+_lib.fda_plan_export_m2l.argtypes = [_P, ctypes.POINTER(_I64), _P, _P, _P]
+_lib.fda_plan_destroy.argtypes = [_P]
+_lib.fda_status_str.argtypes = [ctypes.c_int]
+_lib.fda_status_str.restype = ctypes.c_char_p
+for _f in EXPORTS:
+    if _lib[_f].restype is ctypes.c_int and _f not in ("fda_options_default",):
+        pass
+
+
+class FDAError(RuntimeError):
+    def __init__(self, status, where):
+        super().__init__(f"{where}: {STATUS.get(status, status)}")
+        self.status = status
+
+
+def _check(status, where):
+    if status != FDA_OK:
+        raise FDAError(status, where)
+
+
+def _ptr(a):
+    """Data pointer of a torch tensor or numpy array (must be contiguous)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data_as(ctypes.c_void_p)
+    raise TypeError(type(a))
+
+
+def fda_options_default(**kw) -> fda_options:
+    o = fda_options()
+    _lib.fda_options_default(ctypes.byref(o))
+    for key, v in kw.items():
+        setattr(o, key, v)
+    return o
+
+
+def fda_plan_create(points, normals, quad_weights, k, alpha, eps, options: fda_options | None = None):
+    """Returns an opaque plan handle (ctypes.c_void_p).  points/normals (n,3) float64, weights (n,)."""
+    n = int(points.shape[0])
+    h = _P()
+    a = complex(alpha)
+    if options is None:
+        st = _lib.fda_plan_create(n, _ptr(points), _ptr(normals), _ptr(quad_weights), float(k), a.real, a.imag,
+                                  float(eps), ctypes.byref(h))
+    else:
+        st = _lib.fda_plan_create_ex(n, _ptr(points), _ptr(normals), _ptr(quad_weights), float(k), a.real, a.imag,
+                                     float(eps), ctypes.byref(options), ctypes.byref(h))
+    _check(st, "fda_plan_create")
+    return h
+
+
+def fda_plan_set_correction(plan, row_ptr, col, val):
+    nnz = int(col.shape[0])
+    _check(_lib.fda_plan_set_correction(plan, nnz, _ptr(row_ptr), _ptr(col), _ptr(val)), "fda_plan_set_correction")
+
+
+def fda_apply(plan, phi, out):
+    _check(_lib.fda_apply(plan, _ptr(phi), _ptr(out)), "fda_apply")
+
+
+def fda_apply_phases(plan, mask, phi, out):
+    _check(_lib.fda_apply_phases(plan, int(mask), _ptr(phi), _ptr(out)), "fda_apply_phases")
+
+
+def fda_apply_timed(plan, mask, phi, out):
+    ms = (ctypes.c_float * 9)()
+    _check(_lib.fda_apply_timed(plan, int(mask), _ptr(phi), _ptr(out), ms), "fda_apply_timed")
+    return dict(zip(PHASES, list(ms)))
+
+
+def fda_plan_set_stream(plan, stream_handle: int):
+    _check(_lib.fda_plan_set_stream(plan, ctypes.c_void_p(stream_handle)), "fda_plan_set_stream")
+
+
+def fda_plan_stats(plan) -> dict:
+    s = fda_stats()
+    _check(_lib.fda_plan_stats(plan, ctypes.byref(s)), "fda_plan_stats")
+    return s.as_dict()
+
+
+def fda_plan_log(plan) -> str:
+    return (_lib.fda_plan_log(plan) or b"").decode()
+
+
+def fda_plan_export_leaves(plan, n):
+    nl = _I64()
+    _check(_lib.fda_plan_export_leaves(plan, ctypes.byref(nl), None, None, None), "fda_plan_export_leaves")
+    lop = np.empty(n, np.int32)
+    lev = np.empty(nl.value, np.int32)
+    ijk = np.empty((nl.value, 3), np.int64)
+    _check(_lib.fda_plan_export_leaves(plan, ctypes.byref(nl), _ptr(lop), _ptr(lev), _ptr(ijk)),
+           "fda_plan_export_leaves")
+    return lop, lev, ijk
+
+
+def fda_plan_export_p2p(plan):
+    npairs = _I64()
+    _check(_lib.fda_plan_export_p2p(plan, ctypes.byref(npairs), None, None), "fda_plan_export_p2p")
+    t = np.empty(npairs.value, np.int32)
+    s = np.empty(npairs.value, np.int32)
+    _check(_lib.fda_plan_export_p2p(plan, ctypes.byref(npairs), _ptr(t), _ptr(s)), "fda_plan_export_p2p")
+    return t, s
+
+
+def fda_plan_export_m2l(plan):
+    npairs = _I64()
+    _check(_lib.fda_plan_export_m2l(plan, ctypes.byref(npairs), None, None, None), "fda_plan_export_m2l")
+    lev = np.empty(npairs.value, np.int32)
+    t = np.empty((npairs.value, 3), np.int64)
+    s = np.empty((npairs.value, 3), np.int64)
+    _check(_lib.fda_plan_export_m2l(plan, ctypes.byref(npairs), _ptr(lev), _ptr(t), _ptr(s)), "fda_plan_export_m2l")
+    return lev, t, s
+
+
+def fda_plan_destroy(plan):
+    _check(_lib.fda_plan_destroy(plan), "fda_plan_destroy")
+
+
+def fda_status_str(status: int) -> str:
+    return _lib.fda_status_str(int(status)).decode()
+
+
+class Plan:
+    """Convenience owner of a plan handle (destroyed on close / garbage collection)."""
+
+    def __init__(self, points, normals, quad_weights, k, alpha, eps=1e-4, **options):
+        self.n = int(points.shape[0])
+        opt = fda_options_default(**options) if options else None
+        self.h = fda_plan_create(points, normals, quad_weights, k, alpha, eps, opt)
+
+    def set_correction(self, row_ptr, col, val):
+        fda_plan_set_correction(self.h, row_ptr, col, val)
+
+    def apply(self, phi, out, mask=FDA_PHASE_ALL):
+        if mask == FDA_PHASE_ALL:
+            fda_apply(self.h, phi, out)
+        else:
+            fda_apply_phases(self.h, mask, phi, out)
+        return out
+
+    def apply_timed(self, phi, out, mask=FDA_PHASE_ALL):
+        return fda_apply_timed(self.h, mask, phi, out)
+
+    def stats(self):
+        return fda_plan_stats(self.h)
+
+    def log(self):
+        return fda_plan_log(self.h)
+
+    def close(self):
+        if getattr(self, "h", None) is not None:
+            fda_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

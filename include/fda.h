@@ -125,6 +125,8 @@ fda_status fda_apply_timed(fda_plan plan, uint32_t mask, const double* phi, doub
 fda_status fda_plan_set_stream(fda_plan plan, void* stream);
 fda_status fda_plan_stats(fda_plan plan, fda_stats* stats);
 const char* fda_plan_log(fda_plan plan);
+/* Number of CUDA kernels the last apply on this plan launched (memsets excluded); -1 for a null plan. */
+int64_t fda_plan_launches(fda_plan plan);
 
 /* Diagnostics for the list audit (host arrays; pass NULL arrays to query sizes).
  * leaf_of_point: n (caller order); leaf_level / leaf_ijk: per leaf (ijk: 3 int64). */

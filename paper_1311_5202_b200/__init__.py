@@ -1,7 +1,7 @@
 """B200-native FDA Burton-Miller apply (arXiv 1311.5202): libfda.so + ctypes binding.
 
 The product is the C-ABI library ``libfda.so`` (include/fda.h) built from
-``csrc/`` for sm_100a; ``fda`` is its thin Python binding.  See DESIGN.md.
+``csrc/`` for sm_100a (``python -m paper_1311_5202_b200.build``); its thin Python
+binding is ``paper_1311_5202_b200.fda`` (importing it raises ImportError if the
+library is not built -- there is no fallback).  See DESIGN.md.
 """
-from . import fda  # noqa: F401  (raises ImportError if libfda.so is not built)
-from .fda import Plan  # noqa: F401

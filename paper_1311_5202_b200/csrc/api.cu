@@ -78,6 +78,7 @@ struct fda_plan_s {
   int32_t *m2l_tgt = nullptr, *m2l_src = nullptr;
   fda_stats st{};
   std::string logstr;
+  int64_t last_launches = 0;  // kernels launched by the last apply
 };
 
 namespace {
@@ -559,6 +560,16 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
     fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
     mark(9);
     ck(cudaGetLastError());
+    {
+      int64_t L = 3;  // permute, p2p, unpermute
+      if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
+      if (far) {
+        for (const auto& O : P->lo) L += (O.nleaves > 0) + (O.nleaves_own > 0);
+        for (const auto& T : P->tr) L += (T.n_par > 0) + (T.n_child > 0);
+        for (const auto& D : P->lv) L += D.ngroups > 0;
+      }
+      P->last_launches = L;
+    }
     if (!dout) {
       ck(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(double2), cudaMemcpyDeviceToHost, st));
       ck(cudaStreamSynchronize(st));
@@ -591,6 +602,8 @@ fda_status fda_plan_stats(fda_plan P, fda_stats* s) {
 }
 
 const char* fda_plan_log(fda_plan P) { return P ? P->logstr.c_str() : ""; }
+
+int64_t fda_plan_launches(fda_plan P) { return P ? P->last_launches : -1; }
 
 fda_status fda_plan_export_leaves(fda_plan P, int64_t* nleaves, int32_t* leaf_of_point, int32_t* leaf_level,
                                   int64_t* leaf_ijk) {

@@ -29,7 +29,7 @@ PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute
 EXPORTS = ("fda_options_default", "fda_plan_create", "fda_plan_create_ex", "fda_plan_set_correction", "fda_apply",
            "fda_apply_phases", "fda_apply_timed", "fda_plan_set_stream", "fda_plan_stats", "fda_plan_log",
            "fda_plan_export_leaves", "fda_plan_export_p2p", "fda_plan_export_m2l", "fda_plan_destroy",
-           "fda_status_str")
+           "fda_status_str", "fda_plan_launches")
 
 
 class fda_options(ctypes.Structure):
@@ -74,9 +74,8 @@ _lib.fda_plan_export_m2l.argtypes = [_P, ctypes.POINTER(_I64), _P, _P, _P]
 _lib.fda_plan_destroy.argtypes = [_P]
 _lib.fda_status_str.argtypes = [ctypes.c_int]
 _lib.fda_status_str.restype = ctypes.c_char_p
-for _f in EXPORTS:
-    if _lib[_f].restype is ctypes.c_int and _f not in ("fda_options_default",):
-        pass
+_lib.fda_plan_launches.argtypes = [_P]
+_lib.fda_plan_launches.restype = ctypes.c_int64
 
 
 class FDAError(RuntimeError):
@@ -193,6 +192,10 @@ def fda_plan_export_m2l(plan):
 
 def fda_plan_destroy(plan):
     _check(_lib.fda_plan_destroy(plan), "fda_plan_destroy")
+
+
+def fda_plan_launches(plan) -> int:
+    return int(_lib.fda_plan_launches(plan))
 
 
 def fda_status_str(status: int) -> str:

@@ -1,0 +1,48 @@
+"""The C-ABI library loads and exports every symbol include/fda.h declares (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fda.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fda_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    from paper_1311_5202_b200 import build
+    lib = ctypes.CDLL(build.build())
+    names = _declared()
+    assert len(names) >= 15
+    for nm in names:
+        assert hasattr(lib, nm), nm
+    from paper_1311_5202_b200 import fda
+    assert set(names) == set(fda.EXPORTS)
+
+
+def test_status_strings_and_no_gpu_behaviour():
+    from paper_1311_5202_b200 import fda
+    assert fda.fda_status_str(0) == "FDA_OK"
+    assert fda.fda_status_str(4) == "FDA_ERR_CUDA"
+    assert fda.fda_plan_launches(None) == -1
+    import numpy as np
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    x = np.random.default_rng(0).normal(size=(10, 3))
+    n = x / np.linalg.norm(x, axis=1, keepdims=True)
+    w = np.ones(10)
+    # without a device the product path fails loudly (no CPU fallback)
+    with pytest.raises(fda.FDAError, match="FDA_ERR_CUDA"):
+        fda.fda_plan_create(x, n, w, 1.0, 1j, 1e-4)
+
+
+def test_options_layout():
+    from paper_1311_5202_b200 import fda
+    o = fda.fda_options_default()
+    assert o.lowrank == 1 and o.nranks == 1 and o.lf_p_low == 6 and o.hf_max_rows > 0

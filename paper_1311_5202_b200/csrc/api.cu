@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/fda.h"
@@ -22,18 +23,12 @@ struct DevLevel {
   int64_t n_out = 0, n_in = 0;
   double2* X = nullptr;
   double2* Y = nullptr;
-  // M2L
-  int64_t ngroups = 0;
-  int64_t *gbeg = nullptr, *gend = nullptr, *gmat = nullptr;
-  int32_t* grank = nullptr;
-  double2* pool = nullptr;
+  fda::GTrans m2l;  // H6
 };
 struct DevTrans {
   int lp = 0, sp = 0, sc = 0;
-  double2 *pool = nullptr, *poolT = nullptr;
-  int64_t n_par = 0, n_child = 0;
-  int64_t *up_ptr = nullptr, *dn_ptr = nullptr;
-  int32_t *up_child = nullptr, *up_mat = nullptr, *dn_parent = nullptr, *dn_mat = nullptr;
+  fda::GTrans up;   // H5 M2M: child X -> parent X
+  fda::GTrans dn;   // H7 L2L: parent Y -> child Y
 };
 struct DevLeafOps {
   int level = 0, s = 0, nsurf = 0;
@@ -75,7 +70,6 @@ struct fda_plan_s {
   std::vector<DevLevel> lv;
   std::vector<DevTrans> tr;
   std::vector<DevLeafOps> lo;
-  int32_t *m2l_tgt = nullptr, *m2l_src = nullptr;
   fda_stats st{};
   std::string logstr;
   int64_t last_launches = 0;  // kernels launched by the last apply
@@ -147,6 +141,118 @@ void free_plan(fda_plan P) {
   P->allocs.clear();
 }
 
+// Pairs (out slot, in slot) in group-major order; each group one translation matrix.
+struct GroupedPairs {
+  std::vector<int64_t> gptr{0};
+  std::vector<int64_t> out, in;
+  std::vector<int32_t> rank;
+  std::vector<int64_t> mat;
+};
+
+// Split the output slots into work items that own them exclusively (direction x Morton slab of
+// cubes), so the grouped-translation kernel accumulates without atomics; each item walks its
+// groups in order.  Slab count: enough pairs per (item, group) to amortise the matrix
+// (>= ~32) and enough items to fill the GPU (>= 2 CTAs per SM).
+fda::GTrans make_items(fda_plan P, const GroupedPairs& G, const std::vector<int64_t>& out_cube,
+                       const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, double2* pool) {
+  fda::GTrans T;
+  const int64_t ng = (int64_t)G.rank.size(), np = (int64_t)G.out.size();
+  if (np == 0) return T;
+  std::unordered_map<int, int64_t> dix;
+  for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
+  const int64_t nd = (int64_t)dix.size();
+  const double ppg = (double)np / (double)std::max<int64_t>(ng, 1);
+  // parallelism first (>= 4 items per SM), then >= 32 pairs per (item, group) where the groups allow
+  int64_t S = std::max<int64_t>((int64_t)(ppg / 32), (4 * 148 + nd - 1) / nd);
+  S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
+  int rmax = 0;
+  for (int64_t g = 0; g < ng; ++g) rmax = std::max(rmax, (int)G.rank[g]);
+  if (ppg / (double)S < 24.0) {
+    // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items
+    // (chunks of <= 128 pairs of one group) reuse the matrix; outputs then need atomics.
+    std::vector<int64_t> iptr{0}, igpb, igpe;
+    std::vector<int32_t> igg, order;
+    std::vector<double> cost;
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; p += 128) {
+        const int64_t q = std::min<int64_t>(p + 128, G.gptr[g + 1]);
+        igg.push_back((int32_t)g), igpb.push_back(p), igpe.push_back(q);
+        iptr.push_back((int64_t)igg.size());
+        const int r = G.rank[g];
+        cost.push_back((double)(q - p) * (r < 0 ? (double)s_out * s_in : (double)r * (s_out + s_in)));
+        order.push_back((int32_t)order.size());
+      }
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+    std::vector<int32_t> pout(G.out.begin(), G.out.end()), pin(G.in.begin(), G.in.end());
+    T.n_items = (int64_t)order.size();
+    T.item_order = upload(P, order);
+    T.item_ptr = upload(P, iptr);
+    T.ig_group = upload(P, igg);
+    T.ig_pb = upload(P, igpb);
+    T.ig_pe = upload(P, igpe);
+    T.out = upload(P, pout);
+    T.in = upload(P, pin);
+    T.grank = upload(P, G.rank);
+    T.gmat = upload(P, G.mat);
+    T.pool = pool;
+    T.s_out = s_out, T.s_in = s_in, T.rmax = rmax, T.atomic = 1;
+    return T;
+  }
+  const int64_t nitems = nd * S;
+  std::vector<int64_t> item(np);
+  std::vector<int64_t> cnt(nitems + 1, 0);
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t o = G.out[p];
+    item[p] = dix[out_dir[o]] * S + (out_cube[o] * S) / std::max<int64_t>(ncubes, 1);
+    cnt[item[p] + 1]++;
+  }
+  for (int64_t i = 0; i < nitems; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+  std::vector<int32_t> pout(np), pin(np), pg(np);
+  for (int64_t g = 0; g < ng; ++g)
+    for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; ++p) {
+      const int64_t pos = fill[item[p]]++;
+      pout[pos] = (int32_t)G.out[p];
+      pin[pos] = (int32_t)G.in[p];
+      pg[pos] = (int32_t)g;
+    }
+  std::vector<int64_t> iptr(nitems + 1, 0), igpb, igpe;
+  std::vector<int32_t> igg;
+  std::vector<double> cost(nitems, 0.0);
+  for (int64_t i = 0; i < nitems; ++i) {
+    for (int64_t p = cnt[i]; p < cnt[i + 1];) {
+      int64_t q = p;
+      while (q < cnt[i + 1] && pg[q] == pg[p]) ++q;
+      igg.push_back(pg[p]);
+      igpb.push_back(p);
+      igpe.push_back(q);
+      const int r = G.rank[pg[p]];
+      cost[i] += (double)(q - p) * (r < 0 ? (double)s_out * s_in : (double)r * (s_out + s_in)) + 2000.0;
+      p = q;
+    }
+    iptr[i + 1] = (int64_t)igg.size();
+  }
+  std::vector<int32_t> order;
+  for (int64_t i = 0; i < nitems; ++i)
+    if (cnt[i + 1] > cnt[i]) order.push_back((int32_t)i);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+  T.n_items = (int64_t)order.size();
+  T.item_order = upload(P, order);
+  T.item_ptr = upload(P, iptr);
+  T.ig_group = upload(P, igg);
+  T.ig_pb = upload(P, igpb);
+  T.ig_pe = upload(P, igpe);
+  T.out = upload(P, pout);
+  T.in = upload(P, pin);
+  T.grank = upload(P, G.rank);
+  T.gmat = upload(P, G.mat);
+  T.pool = pool;
+  T.s_out = s_out;
+  T.s_in = s_in;
+  T.rmax = rmax;
+  return T;
+}
+
 fda_status upload_plan(fda_plan P, const fda_options& o) {
   fda::HostPlan& H = P->H;
   const int64_t n = H.n;
@@ -199,53 +305,74 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     if (L.n_out) D.X = dalloc<double2>(P, (size_t)L.n_out * L.s);
     if (L.n_in) D.Y = dalloc<double2>(P, (size_t)L.n_in * L.s);
   }
-  // M2L groups: filter pairs to owned targets
-  {
-    std::vector<int64_t> tg, sr;
-    for (int l = 0; l < nlev; ++l) {
-      const fda::Level& L = H.levels[l];
-      DevLevel& D = P->lv[l];
-      std::vector<int64_t> gb, ge, gm;
-      std::vector<int32_t> gr;
-      for (const auto& G : H.m2l_groups) {
-        if (G.level != l) continue;
-        const int64_t b0 = (int64_t)tg.size();
-        for (int64_t p = G.pbeg; p < G.pend; ++p) {
-          const int64_t ts = H.m2l_tgt[p];
-          if (R > 1 && !owned_cube(L.cubes[L.in_cube[ts]])) continue;
-          tg.push_back(ts);
-          sr.push_back(H.m2l_src[p]);
-        }
-        if ((int64_t)tg.size() == b0) continue;
-        gb.push_back(b0), ge.push_back((int64_t)tg.size()), gm.push_back(G.mat_off), gr.push_back(G.rank);
-        P->st.m2l_pairs += (int64_t)tg.size() - b0;
-        P->st.m2l_groups += 1;
-        P->st.m2l_lowrank_groups += G.rank >= 0;
-        const double np = (double)((int64_t)tg.size() - b0);
-        P->st.flops_m2l += np * (G.rank < 0 ? 8.0 * L.s * L.s : 16.0 * G.rank * L.s);
+  // M2L: pairs filtered to owned targets, grouped by offset, split into owned work items
+  for (int l = 0; l < nlev; ++l) {
+    const fda::Level& L = H.levels[l];
+    GroupedPairs G;
+    for (const auto& g : H.m2l_groups) {
+      if (g.level != l) continue;
+      const size_t b0 = G.out.size();
+      for (int64_t p = g.pbeg; p < g.pend; ++p) {
+        const int64_t ts = H.m2l_tgt[p];
+        if (R > 1 && !owned_cube(L.cubes[L.in_cube[ts]])) continue;
+        G.out.push_back(ts);
+        G.in.push_back(H.m2l_src[p]);
       }
-      D.ngroups = (int64_t)gb.size();
-      if (D.ngroups) {
-        D.gbeg = upload(P, gb), D.gend = upload(P, ge), D.gmat = upload(P, gm), D.grank = upload(P, gr);
-        D.pool = upload_c(P, H.m2l_pool[l]);
-      }
+      if (G.out.size() == b0) continue;
+      G.gptr.push_back((int64_t)G.out.size());
+      G.rank.push_back(g.rank);
+      G.mat.push_back(g.mat_off);
+      const double np = (double)(G.out.size() - b0);
+      P->st.m2l_pairs += (int64_t)np;
+      P->st.m2l_groups += 1;
+      P->st.m2l_lowrank_groups += g.rank >= 0;
+      P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s);
     }
-    P->m2l_tgt = upload_i32(P, tg);
-    P->m2l_src = upload_i32(P, sr);
+    if (G.out.empty()) continue;
+    P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s,
+                              upload_c(P, H.m2l_pool[l]));
   }
-  // transitions
+  // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
+  // L2L items own child in slots (groups = the same matrices, transposed layout)
   for (const auto& T : H.trans) {
     DevTrans D;
+    const fda::Level& Lp = H.levels[T.lp];
+    const fda::Level& Lc = H.levels[T.lp + 1];
     D.lp = T.lp, D.sp = T.sp, D.sc = T.sc;
-    D.pool = upload_c(P, T.pool);
-    D.poolT = upload_c(P, T.poolT);
-    D.n_par = (int64_t)T.up_ptr.size() - 1;
-    D.n_child = (int64_t)T.dn_ptr.size() - 1;
-    std::vector<int64_t> um(T.up_mat.size()), dm(T.dn_mat.size());
-    for (size_t e = 0; e < um.size(); ++e) um[e] = T.mat_index[T.up_mat[e]];
-    for (size_t e = 0; e < dm.size(); ++e) dm[e] = T.mat_index[T.dn_mat[e]];
-    D.up_ptr = upload(P, T.up_ptr), D.up_child = upload_i32(P, T.up_child), D.up_mat = upload_i32(P, um);
-    D.dn_ptr = upload(P, T.dn_ptr), D.dn_parent = upload_i32(P, T.dn_parent), D.dn_mat = upload_i32(P, dm);
+    double2* pool = upload_c(P, T.pool);
+    double2* poolT = upload_c(P, T.poolT);
+    const int64_t nmat = (int64_t)(T.pool.size() / std::max<size_t>(1, (size_t)T.sp * T.sc));
+    auto grouped = [&](const std::vector<int64_t>& ptr, const std::vector<int64_t>& other,
+                       const std::vector<int64_t>& mat) {
+      // CSR by output slot -> group-major pairs
+      GroupedPairs G;
+      std::vector<int64_t> cnt(nmat + 1, 0);
+      for (int64_t m : mat) cnt[T.mat_index[m] + 1]++;
+      for (int64_t g = 0; g < nmat; ++g) cnt[g + 1] += cnt[g];
+      G.out.assign(other.size(), 0);
+      G.in.assign(other.size(), 0);
+      std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+      for (int64_t s = 0; s + 1 < (int64_t)ptr.size(); ++s)
+        for (int64_t e = ptr[s]; e < ptr[s + 1]; ++e) {
+          const int64_t pos = fill[T.mat_index[mat[e]]]++;
+          G.out[pos] = s;
+          G.in[pos] = other[e];
+        }
+      for (int64_t g = 0; g < nmat; ++g) {
+        G.gptr.push_back(cnt[g + 1]);
+        G.rank.push_back(-1);
+        G.mat.push_back(g * (int64_t)T.sp * T.sc);
+      }
+      return G;
+    };
+    if (!T.up_child.empty()) {
+      GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat);
+      D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc, pool);
+    }
+    if (!T.dn_parent.empty()) {
+      GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat);
+      D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp, poolT);
+    }
     P->st.flops_m2m += 8.0 * T.sp * T.sc * (double)T.up_child.size();
     P->st.flops_l2l += 8.0 * T.sp * T.sc * (double)T.dn_parent.size();
     P->tr.push_back(D);
@@ -523,38 +650,57 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       fda::launch_csr(P->pt_b, P->pt_e, P->c_ptr, P->c_col, P->c_val, P->phim, P->outm, st);
     mark(3);
     const bool far = (mask & FDA_PHASE_FAR) && P->H.lmin >= 0;
+    // FDA_TRACE=1: synchronise after every far-field launch and print its wall time (diagnostics only)
+    static const bool trace = getenv("FDA_TRACE") != nullptr;
+    double tlast = now();
+    auto tr = [&](const char* what, int l) {
+      if (!trace) return;
+      ck(cudaStreamSynchronize(st));
+      const double t = now();
+      fprintf(stderr, "[fda trace] %-4s level %d  %.3f ms\n", what, l, 1e3 * (t - tlast));
+      tlast = t;
+    };
     if (far) {
-      for (const auto& O : P->lo)
+      tr("pre", -1);
+      // M2M accumulates into the non-leaf slots: clear every level's outgoing expansions first
+      for (auto& D : P->lv)
+        if (D.n_out) ck(cudaMemsetAsync(D.X, 0, (size_t)D.n_out * D.s * sizeof(double2), st));
+      for (const auto& O : P->lo) {
         fda::launch_s2m(O.nleaves, O.leaf, O.slot, Lg, Pt, P->q, O.surf, O.nsurf, O.S, O.s, k, P->lv[O.level].X, st);
+        tr("s2m", O.level);
+      }
     }
     mark(4);
     if (far) {
       for (int t = (int)P->tr.size() - 1; t >= 0; --t) {
         const DevTrans& T = P->tr[t];
-        fda::launch_m2m(T.n_par, T.up_ptr, T.up_child, T.up_mat, T.pool, T.sp, T.sc, P->lv[T.lp + 1].X,
-                        P->lv[T.lp].X, st);
+        fda::launch_gtrans(T.up, P->lv[T.lp + 1].X, P->lv[T.lp].X, st);
+        tr("m2m", T.lp);
       }
     }
     mark(5);
     if (far) {
       for (auto& D : P->lv)
         if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
-      for (auto& D : P->lv)
-        if (D.ngroups)
-          fda::launch_m2l(D.ngroups, D.gbeg, D.gend, D.grank, D.gmat, P->m2l_tgt, P->m2l_src, D.pool, D.s, D.X, D.Y,
-                          st);
+      for (size_t l = 0; l < P->lv.size(); ++l) {
+        fda::launch_gtrans(P->lv[l].m2l, P->lv[l].X, P->lv[l].Y, st);
+        if (P->lv[l].m2l.n_items) tr("m2l", (int)l);
+      }
     }
     mark(6);
     if (far) {
-      for (const auto& T : P->tr)
-        fda::launch_l2l(T.n_child, T.dn_ptr, T.dn_parent, T.dn_mat, T.poolT, T.sp, T.sc, P->lv[T.lp].Y,
-                        P->lv[T.lp + 1].Y, st);
+      for (const auto& T : P->tr) {
+        fda::launch_gtrans(T.dn, P->lv[T.lp].Y, P->lv[T.lp + 1].Y, st);
+        tr("l2l", T.lp);
+      }
     }
     mark(7);
     if (far) {
-      for (const auto& O : P->lo)
+      for (const auto& O : P->lo) {
         fda::launch_l2t(O.nleaves_own, O.leaf_own, O.slot_own, Lg, Pt, O.surf, O.nsurf, O.T, O.s, k, alpha,
                         P->lv[O.level].Y, P->outm, st);
+        tr("l2t", O.level);
+      }
     }
     mark(8);
     fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
@@ -565,8 +711,8 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
       if (far) {
         for (const auto& O : P->lo) L += (O.nleaves > 0) + (O.nleaves_own > 0);
-        for (const auto& T : P->tr) L += (T.n_par > 0) + (T.n_child > 0);
-        for (const auto& D : P->lv) L += D.ngroups > 0;
+        for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
+        for (const auto& D : P->lv) L += D.m2l.n_items > 0;
       }
       P->last_launches = L;
     }

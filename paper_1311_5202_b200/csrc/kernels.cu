@@ -407,6 +407,127 @@ void launch_m2l(int64_t ngroups, const int64_t* gbeg, const int64_t* gend, const
   k_m2l<<<(unsigned)ngroups, th, sm, st>>>(gbeg, gend, grank, gmat, tgt, src, pool, s, X, Y);
 }
 
+// ---------------------------------------------------------------- grouped translation (H5/H6/H7)
+// Register-tiled complex FP64 GEMM on 128 threads: output tile TM rows x GT_NB pair columns,
+// each thread RM rows x RN columns; A streamed from global through shared memory in
+// GT_KC-deep slices, B (the gathered input vectors) resident in shared memory.
+#define GT_T 128
+#define GT_NB 16
+#define GT_NBP (GT_NB + 1)   // padded column stride of the shared B / T tiles (bank spread)
+#define GT_KC 16
+
+template <int TM, int TX, int RM, int RN>
+__device__ __forceinline__ void gt_tile(const double2* __restrict__ A, int64_t lda, int row0, int M, int K,
+                                        const double2* Bs, double2* As, double2 (&acc)[RM][RN]) {
+  const int tid = threadIdx.x, ty = tid / TX, tx = tid % TX;
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < RN; ++c) acc[r][c] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < K; k0 += GT_KC) {
+    __syncthreads();
+    for (int e = tid; e < GT_KC * TM; e += GT_T) {
+      const int kk = e / TM, i = e % TM;
+      const int row = row0 + i, k = k0 + kk;
+      As[e] = (row < M && k < K) ? __ldg(&A[row + (int64_t)k * lda]) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const int kmax = min(GT_KC, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double2 a[RM], b[RN];
+#pragma unroll
+      for (int r = 0; r < RM; ++r) a[r] = As[kk * TM + ty * RM + r];
+#pragma unroll
+      for (int c = 0; c < RN; ++c) b[c] = Bs[(k0 + kk) * GT_NBP + tx * RN + c];
+#pragma unroll
+      for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int c = 0; c < RN; ++c) cfma(acc[r][c], a[r], b[c]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
+  extern __shared__ double2 gsm[];
+  const int s_in = T.s_in, s_out = T.s_out;
+  double2* Xs = gsm;                              // s_in x NBP
+  double2* Ts = Xs + (size_t)s_in * GT_NBP;       // rmax x NBP
+  double2* As = Ts + (size_t)T.rmax * GT_NBP;     // KC x 64
+  __shared__ int sOut[GT_NB];
+  const int tid = threadIdx.x;
+  const int64_t item = T.item_order[blockIdx.x];
+  for (int64_t e = T.item_ptr[item]; e < T.item_ptr[item + 1]; ++e) {
+    const int g = T.ig_group[e];
+    const int rank = T.grank[g];
+    const double2* Mg = T.pool + T.gmat[g];
+    const int64_t pe = T.ig_pe[e];
+    for (int64_t c0 = T.ig_pb[e]; c0 < pe; c0 += GT_NB) {
+      const int nb = (int)min((int64_t)GT_NB, pe - c0);
+      __syncthreads();
+      if (tid < GT_NB) sOut[tid] = tid < nb ? T.out[c0 + tid] : -1;
+      for (int idx = tid; idx < s_in * GT_NB; idx += GT_T) {
+        const int c = idx / s_in, k = idx - c * s_in;
+        Xs[k * GT_NBP + c] = c < nb ? X[(int64_t)T.in[c0 + c] * s_in + k] : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      const double2* Bs = Xs;
+      const double2* U = Mg;
+      int kin = s_in;
+      if (rank >= 0) {
+        // stage 1: T = Vh (r x s_in) X
+        const double2* Vh = Mg + (int64_t)s_out * rank;
+        for (int row0 = 0; row0 < rank; row0 += 32) {
+          double2 acc[4][1];
+          gt_tile<32, 16, 4, 1>(Vh, rank, row0, rank, s_in, Xs, As, acc);
+          const int ty = tid / 16, tx = tid % 16;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = row0 + ty * 4 + r;
+            if (row < rank) Ts[row * GT_NBP + tx] = acc[r][0];
+          }
+        }
+        __syncthreads();
+        Bs = Ts;
+        kin = rank;
+      }
+      // stage 2 (or dense): Y += A (s_out x kin) B
+      for (int row0 = 0; row0 < s_out; row0 += 64) {
+        double2 acc[4][2];
+        gt_tile<64, 8, 4, 2>(U, s_out, row0, s_out, kin, Bs, As, acc);
+        const int ty = tid / 8, tx = tid % 8;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int col = tx * 2 + c;
+          if (col >= nb) continue;
+          double2* y = Y + (int64_t)sOut[col] * s_out;
+          if (T.atomic) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = row0 + ty * 4 + r;
+              if (row < s_out) {
+                atomicAdd(&y[row].x, acc[r][c].x);
+                atomicAdd(&y[row].y, acc[r][c].y);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = row0 + ty * 4 + r;
+              if (row < s_out) y[row] = cadd(y[row], acc[r][c]);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
+  if (T.n_items <= 0) return;
+  const size_t sm = ((size_t)T.s_in * GT_NBP + (size_t)T.rmax * GT_NBP + (size_t)GT_KC * 64) * sizeof(double2);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_gtrans<<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+}
+
 // ---------------------------------------------------------------- H8 L2T
 #define L2T_T 128
 __global__ void __launch_bounds__(L2T_T) k_l2t(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ slots,

@@ -39,6 +39,27 @@ void launch_l2l(int64_t nchild, const int64_t* dn_ptr, const int32_t* dn_parent,
 void launch_m2l(int64_t ngroups, const int64_t* gbeg, const int64_t* gend, const int32_t* grank,
                 const int64_t* gmat, const int32_t* tgt, const int32_t* src, const double2* pool, int s,
                 const double2* X, double2* Y, cudaStream_t st);
+// Grouped translation (H5 M2M, H6 M2L, H7 L2L): one CTA per work item; an item owns a
+// disjoint set of output slots and walks a list of groups, each group = one matrix
+// (dense s_out x s_in, or low-rank U (s_out x r) Vh (r x s_in)) applied to its pairs:
+//   Y[out_slot] += A X[in_slot]   (no atomics: outputs are owned by the item)
+struct GTrans {
+  int64_t n_items = 0;
+  const int32_t* item_order = nullptr;  // launch order (largest first)
+  const int64_t* item_ptr = nullptr;    // item -> [ig begin, ig end)
+  const int32_t* ig_group = nullptr;    // item-group entry -> group
+  const int64_t* ig_pb = nullptr;       // item-group entry -> pair range
+  const int64_t* ig_pe = nullptr;
+  const int32_t* out = nullptr;         // pair -> output slot
+  const int32_t* in = nullptr;          // pair -> input slot
+  const int32_t* grank = nullptr;       // group -> -1 (dense) or r
+  const int64_t* gmat = nullptr;        // group -> matrix offset (complex elements) into pool
+  const double2* pool = nullptr;
+  int s_out = 0, s_in = 0, rmax = 0;
+  int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
+};
+void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
+
 void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
                 const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha,
                 const double2* Y, double2* outm, cudaStream_t st);

@@ -337,7 +337,8 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     const Level& L = P.levels[l];
     const Level& Lp = P.levels[l - 1];
     const int Rp = Lp.R, Rc = L.R;
-    const int span = 2 * Rp + 1;          // children offsets |delta| <= 2 Rp + 1
+    // children offsets |delta| <= 2 Rp + 1, and never more than the level's grid extent
+    const int span = (int)std::min<int64_t>(2 * Rp + 1, (1LL << l) - 1);
     const int D = 2 * span + 1;
     std::vector<std::vector<PairL>> buckets((size_t)D * D * D);
     const int64_t npar = (int64_t)Lp.cubes.size();
@@ -556,7 +557,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       return t;
     }();
     const int Rp = P.levels[l - 1].R;
-    const int span = 2 * Rp + 1;
+    const int span = (int)std::min<int64_t>(2 * Rp + 1, (1LL << l) - 1);
     const bool parent_slots = (l - 1 >= lmin) && P.levels[l - 1].hf && !P.levels[l - 1].reps.empty();
     std::string err;
 #pragma omp parallel for schedule(dynamic, 1)

@@ -36,9 +36,15 @@ WORKLOADS = {
 }
 
 
-def fp64_peak_tflops(sm_mhz: float) -> float:
-    """FP64 (DFMA) peak from the unit counts: 148 SMs x 64 FP64 FMA/clk x 2 flop."""
-    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+def fp64_peak_tflops(sm_mhz: float):
+    """FP64 roofline peak: the measured DFMA / DMMA figure (profiles/fp64_peak_r01.json, tools/fp64_peak.cu),
+    else derived from the unit counts 148 SM x 64 FP64 FMA/clk x 2 flop x clock."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return max(d["dfma_tflops"], d["dmma_tflops"]), "measured FP64 (tools/fp64_peak.cu: max of DFMA, DMMA)"
+    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12, "derived FP64 DFMA peak: 148 SM x 64 FMA/clk x 2 x sm_max_mhz"
 
 
 def measured_peaks():
@@ -197,6 +203,7 @@ def main():
         step(phases)
     e1.record(stream)
     torch.cuda.synchronize()
+    launches_step = launches_per_step(h)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -262,11 +269,11 @@ def main():
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
                 "traffic": traffic, "kernel": dom, "peak_source": pk_kind}
     else:
-        peak = fp64_peak_tflops(pk.get("sm_max_mhz", 1965.0))
+        peak, peak_src = fp64_peak_tflops(pk.get("sm_max_mhz", 1965.0))
         ach = flops.get(dom, 0.0) / (per[dom] * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                 "traffic": traffic, "kernel": dom,
-                "peak_source": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x sm_max_mhz (derived, DESIGN.md)"}
+                "peak_source": peak_src}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -284,7 +291,7 @@ def main():
                 "plan": {k_: st[k_] for k_ in ("nleaves", "nlevels", "lmin", "p2p_point_pairs", "m2l_pairs",
                                                "m2l_groups", "m2l_lowrank_groups", "out_slots", "in_slots",
                                                "device_bytes")}}
-        line["gpu_launches"] = launches_per_step(h) * args.steps
+        line["gpu_launches"] = launches_step * args.steps
         print(json.dumps(line), flush=True)
     fda.fda_plan_destroy(h)
     if world > 1:

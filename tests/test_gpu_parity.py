@@ -122,7 +122,9 @@ def test_host_pointers_and_linearity(cfg1):
         out_h = np.empty_like(phi)
         fda.fda_apply(h, phi.view(np.float64), out_h.view(np.float64))
         out_d = _run(h, phi)
-        assert np.array_equal(out_h, out_d)
+        # M2L items with few pairs per group accumulate with FP64 atomics: summation order (and so
+        # the last bits) may differ between applies; identical to rounding.
+        assert oracle.rel_l2(out_h, out_d) <= 1e-14
         phi2 = synth.random_phi(p.N, 12)
         a = _run(h, phi)
         b = _run(h, phi2)

@@ -822,11 +822,18 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     for (int l = 0; l < nlev; ++l) {
       const Level& L = P.levels[l];
       int64_t npairs = 0, ngrp = 0, nlow = 0;
+      double fl = 0, rsum = 0;
       for (auto& G : P.m2l_groups)
-        if (G.level == l) npairs += G.pend - G.pbeg, ++ngrp, nlow += G.rank >= 0;
+        if (G.level == l) {
+          const double np = (double)(G.pend - G.pbeg);
+          npairs += G.pend - G.pbeg, ++ngrp, nlow += G.rank >= 0;
+          fl += np * (G.rank < 0 ? 8.0 * L.s * L.s : 16.0 * G.rank * L.s);
+          rsum += np * (G.rank < 0 ? L.s : G.rank);
+        }
       log << "  L" << l << " w/lambda=" << (k > 0 ? L.w / lambda : 0) << (L.hf ? " HF" : " LF") << " R=" << L.R
           << " m=" << L.m << " cubes=" << L.cubes.size() << " s=" << L.s << " out=" << L.n_out << " in=" << L.n_in
-          << " m2l_pairs=" << npairs << " groups=" << ngrp << " lowrank=" << nlow << "\n";
+          << " m2l_pairs=" << npairs << " groups=" << ngrp << " lowrank=" << nlow
+          << " mean_rank=" << (npairs ? rsum / (double)npairs : 0.0) << " m2l_gflop=" << fl * 1e-9 << "\n";
     }
     P.log = log.str();
   }

@@ -60,6 +60,7 @@ struct fda_plan_s {
   int32_t* p2p_src;
   double2 *q, *phim, *outm, *phi_buf, *out_buf;
   // ownership (multi-GPU)
+  int nranks = 1;
   int64_t leaf_b = 0, leaf_e = 0, pt_b = 0, pt_e = 0;
   // correction
   int64_t nnz = 0;
@@ -153,11 +154,58 @@ struct GroupedPairs {
 // cubes), so the grouped-translation kernel accumulates without atomics; each item walks its
 // groups in order.  Slab count: enough pairs per (item, group) to amortise the matrix
 // (>= ~32) and enough items to fill the GPU (>= 2 CTAs per SM).
-fda::GTrans make_items(fda_plan P, const GroupedPairs& G, const std::vector<int64_t>& out_cube,
-                       const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, double2* pool) {
+// Append matrix A (M x K; element (i, j) = a(i, j)) in DMMA fragment order, padded to Mp x Kp
+// (kernels.cuh GTrans): tiles (mt, kt) of 8 x 4, each 32 real parts in lane order then 32 imaginary.
+template <class F>
+void frag_append(std::vector<double>& out, int M, int K, int Mp, int Kp, F a) {
+  for (int mt = 0; mt < Mp / 8; ++mt)
+    for (int kt = 0; kt < Kp / 4; ++kt) {
+      double re[32], im[32];
+      for (int l = 0; l < 32; ++l) {
+        const int i = mt * 8 + l / 4, j = kt * 4 + l % 4;
+        const cplx v = (i < M && j < K) ? a(i, j) : cplx(0.0);
+        re[l] = v.real(), im[l] = v.imag();
+      }
+      out.insert(out.end(), re, re + 32);
+      out.insert(out.end(), im, im + 32);
+    }
+}
+inline int pad8(int v) { return (v + 7) / 8 * 8; }
+inline int pad4(int v) { return (v + 3) / 4 * 4; }
+
+// Fragment-order pool of the groups' matrices.  raw: the plan's column-major pool; a dense group is
+// s_out x s_in (ld s_out) at G.mat[g]; a low-rank group is U (s_out x r, ld s_out) then V (r x s_in, ld r).
+// Rewrites G.mat to offsets (doubles) into the returned pool.
+std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s_in, int* rmax8) {
+  std::vector<double> pool;
+  *rmax8 = 0;
+  for (size_t g = 0; g < G.rank.size(); ++g) {
+    const cplx* A = raw + G.mat[g];
+    const int r = G.rank[g];
+    G.mat[g] = (int64_t)pool.size();
+    if (r < 0) {
+      frag_append(pool, s_out, s_in, pad8(s_out), pad4(s_in), [&](int i, int j) { return A[i + (int64_t)j * s_out]; });
+    } else {
+      const cplx* V = A + (int64_t)s_out * r;
+      frag_append(pool, r, s_in, pad8(r), pad4(s_in), [&](int i, int j) { return V[i + (int64_t)j * r]; });
+      frag_append(pool, s_out, r, pad8(s_out), pad8(r), [&](int i, int j) { return A[i + (int64_t)j * s_out]; });
+      *rmax8 = std::max(*rmax8, pad8(r));
+    }
+  }
+  return pool;
+}
+
+fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& out_cube,
+                       const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, const cplx* raw) {
   fda::GTrans T;
   const int64_t ng = (int64_t)G.rank.size(), np = (int64_t)G.out.size();
   if (np == 0) return T;
+  {
+    int rmax8 = 0;
+    std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8);
+    T.pool = upload(P, pool);
+    T.rmax8 = rmax8;
+  }
   std::unordered_map<int, int64_t> dix;
   for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
   const int64_t nd = (int64_t)dix.size();
@@ -165,8 +213,6 @@ fda::GTrans make_items(fda_plan P, const GroupedPairs& G, const std::vector<int6
   // parallelism first (>= 4 items per SM), then >= 32 pairs per (item, group) where the groups allow
   int64_t S = std::max<int64_t>((int64_t)(ppg / 32), (4 * 148 + nd - 1) / nd);
   S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
-  int rmax = 0;
-  for (int64_t g = 0; g < ng; ++g) rmax = std::max(rmax, (int)G.rank[g]);
   if (ppg / (double)S < 24.0) {
     // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items
     // (chunks of <= 128 pairs of one group) reuse the matrix; outputs then need atomics.
@@ -194,8 +240,7 @@ fda::GTrans make_items(fda_plan P, const GroupedPairs& G, const std::vector<int6
     T.in = upload(P, pin);
     T.grank = upload(P, G.rank);
     T.gmat = upload(P, G.mat);
-    T.pool = pool;
-    T.s_out = s_out, T.s_in = s_in, T.rmax = rmax, T.atomic = 1;
+    T.s_out = s_out, T.s_in = s_in, T.atomic = 1;
     return T;
   }
   const int64_t nitems = nd * S;
@@ -246,11 +291,34 @@ fda::GTrans make_items(fda_plan P, const GroupedPairs& G, const std::vector<int6
   T.in = upload(P, pin);
   T.grank = upload(P, G.rank);
   T.gmat = upload(P, G.mat);
-  T.pool = pool;
   T.s_out = s_out;
   T.s_in = s_in;
-  T.rmax = rmax;
   return T;
+}
+
+// Ownership (multi-GPU): rank r of R owns the contiguous leaf range whose points
+// start at or after floor(n r / R) and before floor(n (r+1) / R) (leaves are never split).
+void set_ownership(fda_plan P, const fda_options& o) {
+  const fda::HostPlan& H = P->H;
+  const int64_t n = H.n, nl = (int64_t)H.leaves.size();
+  std::vector<int64_t> lp(nl + 1, 0);
+  for (int64_t t = 0; t < nl; ++t) lp[t] = H.cubes[H.leaves[t]].pbeg;
+  lp[nl] = n;
+  const int R = std::max(1, o.nranks), r = std::min(std::max(0, o.rank), R - 1);
+  const int64_t pb = (n * r) / R, pe = (n * (r + 1)) / R;
+  int64_t lb = std::lower_bound(lp.begin(), lp.begin() + nl, pb) - lp.begin();
+  int64_t le = std::lower_bound(lp.begin(), lp.begin() + nl, pe) - lp.begin();
+  if (r == R - 1) le = nl;
+  if (r == 0) lb = 0;
+  P->nranks = R;
+  P->nleaf = nl;
+  P->leaf_b = lb, P->leaf_e = le;
+  P->pt_b = lp[lb], P->pt_e = lp[le];
+  P->st.owned_begin = P->pt_b, P->st.owned_end = P->pt_e;
+  P->st.n = n;
+  P->st.nleaves = nl;
+  P->st.nlevels = (int64_t)H.levels.size();
+  P->st.lmin = H.lmin;
 }
 
 fda_status upload_plan(fda_plan P, const fda_options& o) {
@@ -280,17 +348,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   P->p2p_src = upload_i32(P, H.p2p_src);
   P->q = dalloc<double2>(P, n), P->phim = dalloc<double2>(P, n), P->outm = dalloc<double2>(P, n);
   P->phi_buf = dalloc<double2>(P, n), P->out_buf = dalloc<double2>(P, n);
-  // ownership: contiguous leaf range balanced by points (multi-GPU)
-  const int R = std::max(1, o.nranks), r = std::min(std::max(0, o.rank), R - 1);
-  {
-    const int64_t pb = (n * r) / R, pe = (n * (r + 1)) / R;
-    int64_t lb = std::lower_bound(lp.begin(), lp.begin() + nl, pb) - lp.begin();
-    int64_t le = std::lower_bound(lp.begin(), lp.begin() + nl, pe) - lp.begin();
-    if (r == R - 1) le = nl;
-    if (r == 0) lb = 0;
-    P->leaf_b = lb, P->leaf_e = le;
-    P->pt_b = lp[lb], P->pt_e = lp[le];
-  }
+  const int R = P->nranks;
   auto owned_cube = [&](int64_t gid) {
     const fda::Cube& c = H.cubes[gid];
     return c.pend > P->pt_b && c.pbeg < P->pt_e;
@@ -329,8 +387,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s);
     }
     if (G.out.empty()) continue;
-    P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s,
-                              upload_c(P, H.m2l_pool[l]));
+    P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
   }
   // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
   // L2L items own child in slots (groups = the same matrices, transposed layout)
@@ -339,8 +396,6 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const fda::Level& Lp = H.levels[T.lp];
     const fda::Level& Lc = H.levels[T.lp + 1];
     D.lp = T.lp, D.sp = T.sp, D.sc = T.sc;
-    double2* pool = upload_c(P, T.pool);
-    double2* poolT = upload_c(P, T.poolT);
     const int64_t nmat = (int64_t)(T.pool.size() / std::max<size_t>(1, (size_t)T.sp * T.sc));
     auto grouped = [&](const std::vector<int64_t>& ptr, const std::vector<int64_t>& other,
                        const std::vector<int64_t>& mat) {
@@ -367,11 +422,11 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     };
     if (!T.up_child.empty()) {
       GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat);
-      D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc, pool);
+      D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc, T.pool.data());
     }
     if (!T.dn_parent.empty()) {
       GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat);
-      D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp, poolT);
+      D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp, T.poolT.data());
     }
     P->st.flops_m2m += 8.0 * T.sp * T.sc * (double)T.up_child.size();
     P->st.flops_l2l += 8.0 * T.sp * T.sc * (double)T.dn_parent.size();
@@ -508,6 +563,7 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     if (!err.empty()) return FDA_ERR_INVALID_ARG;
     P->host_only = o.host_only != 0;
     P->logstr = P->H.log;
+    set_ownership(P.get(), o);
     if (P->host_only) {
       *out = P.release();
       return FDA_OK;

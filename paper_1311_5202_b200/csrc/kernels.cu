@@ -277,255 +277,156 @@ void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, 
   k_s2m<<<(unsigned)nleaves, S2M_T, nsurf * sizeof(double2), st>>>(leaf_ids, slots, L, P, q, surf, nsurf, S, s, k, X);
 }
 
-// ---------------------------------------------------------------- H5 M2M / H7 L2L
-__global__ void k_m2m(const int64_t* __restrict__ up_ptr, const int32_t* __restrict__ up_child,
-                      const int32_t* __restrict__ up_mat, const double2* __restrict__ pool, int sp, int sc,
-                      const double2* __restrict__ Xc, double2* __restrict__ Xp) {
-  extern __shared__ double2 xs[];
-  const int64_t slot = blockIdx.x;
-  const int i = threadIdx.x;
-  // a leaf's slot has no children: its expansion came from S2M, leave it alone
-  if (up_ptr[slot] == up_ptr[slot + 1]) return;
-  double2 acc = make_double2(0.0, 0.0);
-  const int64_t msz = (int64_t)sp * sc;
-  for (int64_t e = up_ptr[slot]; e < up_ptr[slot + 1]; ++e) {
-    const int64_t c = up_child[e];
-    const double2* M = pool + up_mat[e] * msz;
-    __syncthreads();
-    for (int j = threadIdx.x; j < sc; j += blockDim.x) xs[j] = Xc[c * sc + j];
-    __syncthreads();
-    if (i < sp)
-      for (int j = 0; j < sc; ++j) cfma(acc, M[i + (int64_t)j * sp], xs[j]);
-  }
-  if (i < sp) Xp[slot * sp + i] = acc;
-}
-void launch_m2m(int64_t nparent, const int64_t* up_ptr, const int32_t* up_child, const int32_t* up_mat,
-                const double2* pool, int sp, int sc, const double2* Xc, double2* Xp, cudaStream_t st) {
-  if (nparent <= 0) return;
-  const int th = ((sp + 31) / 32) * 32;
-  k_m2m<<<(unsigned)nparent, th, sc * sizeof(double2), st>>>(up_ptr, up_child, up_mat, pool, sp, sc, Xc, Xp);
-}
-
-__global__ void k_l2l(const int64_t* __restrict__ dn_ptr, const int32_t* __restrict__ dn_parent,
-                      const int32_t* __restrict__ dn_mat, const double2* __restrict__ poolT, int sp, int sc,
-                      const double2* __restrict__ Yp, double2* __restrict__ Yc) {
-  extern __shared__ double2 ys[];
-  const int64_t slot = blockIdx.x;
-  const int j = threadIdx.x;
-  double2 acc = make_double2(0.0, 0.0);
-  const int64_t msz = (int64_t)sp * sc;
-  for (int64_t e = dn_ptr[slot]; e < dn_ptr[slot + 1]; ++e) {
-    const int64_t p = dn_parent[e];
-    const double2* M = poolT + dn_mat[e] * msz;  // sc x sp column-major (= M~^T)
-    __syncthreads();
-    for (int i = threadIdx.x; i < sp; i += blockDim.x) ys[i] = Yp[p * sp + i];
-    __syncthreads();
-    if (j < sc)
-      for (int i = 0; i < sp; ++i) cfma(acc, M[j + (int64_t)i * sc], ys[i]);
-  }
-  if (j < sc) Yc[slot * sc + j] = cadd(Yc[slot * sc + j], acc);
-}
-void launch_l2l(int64_t nchild, const int64_t* dn_ptr, const int32_t* dn_parent, const int32_t* dn_mat,
-                const double2* poolT, int sp, int sc, const double2* Yp, double2* Yc, cudaStream_t st) {
-  if (nchild <= 0) return;
-  const int th = ((sc + 31) / 32) * 32;
-  k_l2l<<<(unsigned)nchild, th, sp * sizeof(double2), st>>>(dn_ptr, dn_parent, dn_mat, poolT, sp, sc, Yp, Yc);
-}
-
-// ---------------------------------------------------------------- H6 M2L (group = one offset)
-#define M2L_PB 8
-__global__ void k_m2l(const int64_t* __restrict__ gbeg, const int64_t* __restrict__ gend,
-                      const int32_t* __restrict__ grank, const int64_t* __restrict__ gmat,
-                      const int32_t* __restrict__ tgt, const int32_t* __restrict__ src,
-                      const double2* __restrict__ pool, int s, const double2* __restrict__ X, double2* __restrict__ Y) {
-  extern __shared__ double2 sm[];
-  double2* xs = sm;                 // PB x s
-  double2* ts = sm + M2L_PB * s;    // PB x s (low-rank intermediate)
-  const int64_t g = blockIdx.x;
-  const int rank = grank[g];
-  const double2* M = pool + gmat[g];
-  const int i = threadIdx.x;
-  for (int64_t p0 = gbeg[g]; p0 < gend[g]; p0 += M2L_PB) {
-    const int np = (int)min((int64_t)M2L_PB, gend[g] - p0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < np * s; e += blockDim.x) {
-      const int pp = e / s, j = e % s;
-      xs[pp * s + j] = X[(int64_t)src[p0 + pp] * s + j];
-    }
-    __syncthreads();
-    double2 y[M2L_PB];
-#pragma unroll
-    for (int pp = 0; pp < M2L_PB; ++pp) y[pp] = make_double2(0.0, 0.0);
-    if (rank < 0) {
-      if (i < s) {
-        for (int j = 0; j < s; ++j) {
-          const double2 m = M[i + (int64_t)j * s];
-#pragma unroll
-          for (int pp = 0; pp < M2L_PB; ++pp) cfma(y[pp], m, xs[pp * s + j]);
-        }
-      }
-    } else {
-      const double2* U = M;                      // s x rank
-      const double2* Vh = M + (int64_t)s * rank; // rank x s
-      if (i < rank) {
-        double2 t[M2L_PB];
-#pragma unroll
-        for (int pp = 0; pp < M2L_PB; ++pp) t[pp] = make_double2(0.0, 0.0);
-        for (int j = 0; j < s; ++j) {
-          const double2 m = Vh[i + (int64_t)j * rank];
-#pragma unroll
-          for (int pp = 0; pp < M2L_PB; ++pp) cfma(t[pp], m, xs[pp * s + j]);
-        }
-#pragma unroll
-        for (int pp = 0; pp < M2L_PB; ++pp) ts[pp * s + i] = t[pp];
-      }
-      __syncthreads();
-      if (i < s) {
-        for (int c = 0; c < rank; ++c) {
-          const double2 m = U[i + (int64_t)c * s];
-#pragma unroll
-          for (int pp = 0; pp < M2L_PB; ++pp) cfma(y[pp], m, ts[pp * s + c]);
-        }
-      }
-    }
-    if (i < s) {
-      for (int pp = 0; pp < np; ++pp) {
-        double* dst = reinterpret_cast<double*>(Y + (int64_t)tgt[p0 + pp] * s + i);
-        atomicAdd(dst, y[pp].x);
-        atomicAdd(dst + 1, y[pp].y);
-      }
-    }
-  }
-}
-void launch_m2l(int64_t ngroups, const int64_t* gbeg, const int64_t* gend, const int32_t* grank, const int64_t* gmat,
-                const int32_t* tgt, const int32_t* src, const double2* pool, int s, const double2* X, double2* Y,
-                cudaStream_t st) {
-  if (ngroups <= 0) return;
-  const int th = ((s + 31) / 32) * 32;
-  const size_t sm = 2 * M2L_PB * s * sizeof(double2);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_m2l<<<(unsigned)ngroups, th, sm, st>>>(gbeg, gend, grank, gmat, tgt, src, pool, s, X, Y);
-}
-
 // ---------------------------------------------------------------- grouped translation (H5/H6/H7)
-// Register-tiled complex FP64 GEMM on 128 threads: output tile TM rows x GT_NB pair columns,
-// each thread RM rows x RN columns; A streamed from global through shared memory in
-// GT_KC-deep slices, B (the gathered input vectors) resident in shared memory.
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) complex GEMM per (item, group, chunk of GT_P pairs):
+//   dense   : Y[out] += A X[in]                  A  : s_out x s_in
+//   low rank: Y[out] += U (V X[in])               V  : r x s_in,  U : s_out x r      (eq_lrdk)
+// Complex products by the 3M scheme: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
+// re = P1 - P2, im = P3 - P1 - P2 (3 real MMAs per complex MMA instead of 4).
+// Matrices live in global memory in fragment order (api.cu frag_append): tile (mt, kt) of 8 x 4
+// holds 32 real parts in lane order (lane -> row mt*8 + lane/4, col kt*4 + lane%4) then 32
+// imaginary parts, so each A-fragment load of a warp is one coalesced 256-byte read (L2 / L1).
+// The gathered input columns X (and the low-rank intermediate T) are B operands in shared memory,
+// planar re / im, column-major with a leading dimension = 4 (mod 16) (conflict-free fragments).
 #define GT_T 128
-#define GT_NB 16
-#define GT_NBP (GT_NB + 1)   // padded column stride of the shared B / T tiles (bank spread)
-#define GT_KC 16
+#define GT_CT 2   // 8-column tiles per warp unit (GT_P: pair columns per chunk, 16 or 32)
 
-template <int TM, int TX, int RM, int RN>
-__device__ __forceinline__ void gt_tile(const double2* __restrict__ A, int64_t lda, int row0, int M, int K,
-                                        const double2* Bs, double2* As, double2 (&acc)[RM][RN]) {
-  const int tid = threadIdx.x, ty = tid / TX, tx = tid % TX;
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 11) / 16) * 16 + 4; }  // >= k, = 4 mod 16
+
+// One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem planes).
+// mode 0: write C into the smem planes Tr/Ti (ldt); mode 1: Y[sOut[col]*s_out + row] += C (plain RMW);
+// mode 2: same with atomics.
+template <int GT_P, int MODE>
+__device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, const double* Br,
+                                         const double* Bi, int ldb, double* Tr, double* Ti, int ldt,
+                                         double2* __restrict__ Y, const int* sOut, int s_out, int nb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int CG = GT_P / 8 / GT_CT;
+  const int nunits = Mt * CG;
+  const int g = lane >> 2, t = lane & 3;
+  for (int u = warp; u < nunits; u += GT_T / 32) {
+    const int mt = u / CG, cg = u - mt * CG;
+    double acc[GT_CT][3][2];
 #pragma unroll
-  for (int r = 0; r < RM; ++r)
+    for (int c = 0; c < GT_CT; ++c)
 #pragma unroll
-    for (int c = 0; c < RN; ++c) acc[r][c] = make_double2(0.0, 0.0);
-  for (int k0 = 0; k0 < K; k0 += GT_KC) {
-    __syncthreads();
-    for (int e = tid; e < GT_KC * TM; e += GT_T) {
-      const int kk = e / TM, i = e % TM;
-      const int row = row0 + i, k = k0 + kk;
-      As[e] = (row < M && k < K) ? __ldg(&A[row + (int64_t)k * lda]) : make_double2(0.0, 0.0);
+      for (int q = 0; q < 3; ++q) acc[c][q][0] = acc[c][q][1] = 0.0;
+    const double* ap = Ag + (size_t)mt * Kt * 64 + lane;
+    const int boff = (cg * GT_CT * 8 + g) * ldb + t;
+#pragma unroll 4
+    for (int kt = 0; kt < Kt; ++kt) {
+      const double ar = __ldg(ap + kt * 64), ai = __ldg(ap + kt * 64 + 32);
+      const double as = ar + ai;
+#pragma unroll
+      for (int c = 0; c < GT_CT; ++c) {
+        const double br = Br[boff + c * 8 * ldb + kt * 4], bi = Bi[boff + c * 8 * ldb + kt * 4];
+        dmma(acc[c][0][0], acc[c][0][1], ar, br);
+        dmma(acc[c][1][0], acc[c][1][1], ai, bi);
+        dmma(acc[c][2][0], acc[c][2][1], as, br + bi);
+      }
     }
-    __syncthreads();
-    const int kmax = min(GT_KC, K - k0);
-    for (int kk = 0; kk < kmax; ++kk) {
-      double2 a[RM], b[RN];
+    const int row = mt * 8 + g;
 #pragma unroll
-      for (int r = 0; r < RM; ++r) a[r] = As[kk * TM + ty * RM + r];
+    for (int c = 0; c < GT_CT; ++c)
 #pragma unroll
-      for (int c = 0; c < RN; ++c) b[c] = Bs[(k0 + kk) * GT_NBP + tx * RN + c];
-#pragma unroll
-      for (int r = 0; r < RM; ++r)
-#pragma unroll
-        for (int c = 0; c < RN; ++c) cfma(acc[r][c], a[r], b[c]);
-    }
+      for (int i = 0; i < 2; ++i) {
+        const int col = (cg * GT_CT + c) * 8 + 2 * t + i;
+        const double re = acc[c][0][i] - acc[c][1][i];
+        const double im = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
+        if (MODE == 0) {
+          Tr[col * ldt + row] = re;
+          Ti[col * ldt + row] = im;
+        } else if (row < s_out && col < nb) {
+          double2* y = Y + (int64_t)sOut[col] * s_out + row;
+          if (MODE == 2) {
+            atomicAdd(&y->x, re);
+            atomicAdd(&y->y, im);
+          } else {
+            double2 v = *y;
+            v.x += re;
+            v.y += im;
+            *y = v;
+          }
+        }
+      }
   }
 }
 
+template <int GT_P>
 __global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
-  extern __shared__ double2 gsm[];
+  extern __shared__ double gsm[];
   const int s_in = T.s_in, s_out = T.s_out;
-  double2* Xs = gsm;                              // s_in x NBP
-  double2* Ts = Xs + (size_t)s_in * GT_NBP;       // rmax x NBP
-  double2* As = Ts + (size_t)T.rmax * GT_NBP;     // KC x 64
-  __shared__ int sOut[GT_NB];
+  const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
+  const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
+  double* Xr = gsm;
+  double* Xi = Xr + GT_P * ldx;
+  double* Tr = Xi + GT_P * ldx;
+  double* Ti = Tr + GT_P * ldt;
+  __shared__ int sOut[GT_P];
   const int tid = threadIdx.x;
   const int64_t item = T.item_order[blockIdx.x];
+  const int kp = kin * 4;
   for (int64_t e = T.item_ptr[item]; e < T.item_ptr[item + 1]; ++e) {
-    const int g = T.ig_group[e];
-    const int rank = T.grank[g];
-    const double2* Mg = T.pool + T.gmat[g];
+    const int grp = T.ig_group[e];
+    const int rank = T.grank[grp];
+    const double* Mg = T.pool + T.gmat[grp];
     const int64_t pe = T.ig_pe[e];
-    for (int64_t c0 = T.ig_pb[e]; c0 < pe; c0 += GT_NB) {
-      const int nb = (int)min((int64_t)GT_NB, pe - c0);
+    for (int64_t c0 = T.ig_pb[e]; c0 < pe; c0 += GT_P) {
+      const int nb = (int)min((int64_t)GT_P, pe - c0);
       __syncthreads();
-      if (tid < GT_NB) sOut[tid] = tid < nb ? T.out[c0 + tid] : -1;
-      for (int idx = tid; idx < s_in * GT_NB; idx += GT_T) {
-        const int c = idx / s_in, k = idx - c * s_in;
-        Xs[k * GT_NBP + c] = c < nb ? X[(int64_t)T.in[c0 + c] * s_in + k] : make_double2(0.0, 0.0);
+      if (tid < GT_P) sOut[tid] = tid < nb ? T.out[c0 + tid] : 0;
+      for (int idx = tid; idx < GT_P * kp; idx += GT_T) {
+        const int c = idx / kp, k = idx - c * kp;
+        double2 v = make_double2(0.0, 0.0);
+        if (c < nb && k < s_in) v = X[(int64_t)T.in[c0 + c] * s_in + k];
+        Xr[c * ldx + k] = v.x;
+        Xi[c * ldx + k] = v.y;
       }
       __syncthreads();
-      const double2* Bs = Xs;
-      const double2* U = Mg;
-      int kin = s_in;
       if (rank >= 0) {
-        // stage 1: T = Vh (r x s_in) X
-        const double2* Vh = Mg + (int64_t)s_out * rank;
-        for (int row0 = 0; row0 < rank; row0 += 32) {
-          double2 acc[4][1];
-          gt_tile<32, 16, 4, 1>(Vh, rank, row0, rank, s_in, Xs, As, acc);
-          const int ty = tid / 16, tx = tid % 16;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = row0 + ty * 4 + r;
-            if (row < rank) Ts[row * GT_NBP + tx] = acc[r][0];
-          }
-        }
+        const int rt = (rank + 7) / 8;  // m tiles of V = k-tile pairs of U
+        gt_stage<GT_P, 0>(Mg, rt, kin, Xr, Xi, ldx, Tr, Ti, ldt, nullptr, nullptr, 0, 0);
         __syncthreads();
-        Bs = Ts;
-        kin = rank;
-      }
-      // stage 2 (or dense): Y += A (s_out x kin) B
-      for (int row0 = 0; row0 < s_out; row0 += 64) {
-        double2 acc[4][2];
-        gt_tile<64, 8, 4, 2>(U, s_out, row0, s_out, kin, Bs, As, acc);
-        const int ty = tid / 8, tx = tid % 8;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int col = tx * 2 + c;
-          if (col >= nb) continue;
-          double2* y = Y + (int64_t)sOut[col] * s_out;
-          if (T.atomic) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int row = row0 + ty * 4 + r;
-              if (row < s_out) {
-                atomicAdd(&y[row].x, acc[r][c].x);
-                atomicAdd(&y[row].y, acc[r][c].y);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int row = row0 + ty * 4 + r;
-              if (row < s_out) y[row] = cadd(y[row], acc[r][c]);
-            }
-          }
-        }
+        const double* U = Mg + (size_t)rt * kin * 64;
+        if (T.atomic)
+          gt_stage<GT_P, 2>(U, mout, 2 * rt, Tr, Ti, ldt, nullptr, nullptr, 0, Y, sOut, s_out, nb);
+        else
+          gt_stage<GT_P, 1>(U, mout, 2 * rt, Tr, Ti, ldt, nullptr, nullptr, 0, Y, sOut, s_out, nb);
+      } else {
+        if (T.atomic)
+          gt_stage<GT_P, 2>(Mg, mout, kin, Xr, Xi, ldx, nullptr, nullptr, 0, Y, sOut, s_out, nb);
+        else
+          gt_stage<GT_P, 1>(Mg, mout, kin, Xr, Xi, ldx, nullptr, nullptr, 0, Y, sOut, s_out, nb);
       }
     }
   }
 }
+
+static size_t gt_smem_p(const GTrans& T, int p) {
+  const int kin = (T.s_in + 3) / 4;
+  return (size_t)(2 * p * gt_ld(kin * 4) + 2 * p * gt_ld(T.rmax8)) * sizeof(double);
+}
+// 32 pair columns per chunk when the tiles are small, else 16 (>= 2 CTAs per SM)
+static int gt_cols(const GTrans& T) { return gt_smem_p(T, 32) <= 100 * 1024 ? 32 : 16; }
+size_t gtrans_smem(const GTrans& T) { return gt_smem_p(T, gt_cols(T)); }
+
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return;
-  const size_t sm = ((size_t)T.s_in * GT_NBP + (size_t)T.rmax * GT_NBP + (size_t)GT_KC * 64) * sizeof(double2);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_gtrans<<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  const int p = gt_cols(T);
+  const size_t sm = gt_smem_p(T, p);
+  if (p == 32) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_gtrans<32><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  } else {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_gtrans<16><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  }
 }
 
 // ---------------------------------------------------------------- H8 L2T

@@ -32,17 +32,12 @@ void launch_csr(int64_t row_begin, int64_t row_end, const int64_t* rp, const int
 void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
                 const double2* q, const double* surf /* nsurf x 3, relative */, int nsurf, const double2* S,
                 int s, double k, double2* X, cudaStream_t st);
-void launch_m2m(int64_t nparent, const int64_t* up_ptr, const int32_t* up_child, const int32_t* up_mat,
-                const double2* pool, int sp, int sc, const double2* Xc, double2* Xp, cudaStream_t st);
-void launch_l2l(int64_t nchild, const int64_t* dn_ptr, const int32_t* dn_parent, const int32_t* dn_mat,
-                const double2* poolT, int sp, int sc, const double2* Yp, double2* Yc, cudaStream_t st);
-void launch_m2l(int64_t ngroups, const int64_t* gbeg, const int64_t* gend, const int32_t* grank,
-                const int64_t* gmat, const int32_t* tgt, const int32_t* src, const double2* pool, int s,
-                const double2* X, double2* Y, cudaStream_t st);
 // Grouped translation (H5 M2M, H6 M2L, H7 L2L): one CTA per work item; an item owns a
 // disjoint set of output slots and walks a list of groups, each group = one matrix
-// (dense s_out x s_in, or low-rank U (s_out x r) Vh (r x s_in)) applied to its pairs:
+// (dense s_out x s_in, or low-rank U (s_out x r) V (r x s_in)) applied to its pairs:
 //   Y[out_slot] += A X[in_slot]   (no atomics: outputs are owned by the item)
+// Matrices are stored in DMMA fragment order (8x4 tiles, 32 re then 32 im doubles per tile,
+// tiles row-tile-major); a low-rank group stores V (pad8(r) x pad4(s_in)) then U (pad8(s_out) x pad8(r)).
 struct GTrans {
   int64_t n_items = 0;
   const int32_t* item_order = nullptr;  // launch order (largest first)
@@ -53,12 +48,13 @@ struct GTrans {
   const int32_t* out = nullptr;         // pair -> output slot
   const int32_t* in = nullptr;          // pair -> input slot
   const int32_t* grank = nullptr;       // group -> -1 (dense) or r
-  const int64_t* gmat = nullptr;        // group -> matrix offset (complex elements) into pool
-  const double2* pool = nullptr;
-  int s_out = 0, s_in = 0, rmax = 0;
+  const int64_t* gmat = nullptr;        // group -> matrix offset (doubles) into pool
+  const double* pool = nullptr;         // fragment-order matrices
+  int s_out = 0, s_in = 0, rmax8 = 0;   // rmax8: largest low rank rounded up to 8
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
 };
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
+size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
 
 void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
                 const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha,

@@ -91,6 +91,7 @@ typedef struct {
   int64_t csr_nnz;
   int64_t device_bytes;
   int64_t owned_begin, owned_end; /* owned points, Morton order */
+  int64_t owned_leaf_begin, owned_leaf_end; /* owned leaves (Morton leaf ids of fda_plan_export_leaves) */
   double setup_tree_s, setup_lists_s, setup_ops_s, setup_upload_s;
   double flops_p2p, flops_m2l, flops_m2m, flops_l2l, flops_s2m, flops_l2t; /* algorithmic flops per apply */
   double bytes_csr;                                                        /* algorithmic bytes of H3 per apply */

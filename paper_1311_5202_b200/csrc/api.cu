@@ -205,15 +205,17 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8);
     T.pool = upload(P, pool);
     T.rmax8 = rmax8;
+    T.s_out = s_out, T.s_in = s_in;
   }
+  const int cols = fda::gtrans_cols(T);
   std::unordered_map<int, int64_t> dix;
   for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
   const int64_t nd = (int64_t)dix.size();
   const double ppg = (double)np / (double)std::max<int64_t>(ng, 1);
-  // parallelism first (>= 4 items per SM), then >= 32 pairs per (item, group) where the groups allow
-  int64_t S = std::max<int64_t>((int64_t)(ppg / 32), (4 * 148 + nd - 1) / nd);
+  // parallelism first (>= 8 items per SM), then ~2 chunks of pairs per (item, group) where the groups allow
+  int64_t S = std::max<int64_t>((int64_t)(ppg / (2 * cols)), (8 * 148 + nd - 1) / nd);
   S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
-  if (ppg / (double)S < 24.0) {
+  if (ppg / (double)S < 0.75 * cols) {
     // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items
     // (chunks of <= 128 pairs of one group) reuse the matrix; outputs then need atomics.
     std::vector<int64_t> iptr{0}, igpb, igpe;
@@ -315,6 +317,7 @@ void set_ownership(fda_plan P, const fda_options& o) {
   P->leaf_b = lb, P->leaf_e = le;
   P->pt_b = lp[lb], P->pt_e = lp[le];
   P->st.owned_begin = P->pt_b, P->st.owned_end = P->pt_e;
+  P->st.owned_leaf_begin = lb, P->st.owned_leaf_end = le;
   P->st.n = n;
   P->st.nleaves = nl;
   P->st.nlevels = (int64_t)H.levels.size();

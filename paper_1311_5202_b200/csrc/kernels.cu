@@ -287,7 +287,9 @@ void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, 
 // holds 32 real parts in lane order (lane -> row mt*8 + lane/4, col kt*4 + lane%4) then 32
 // imaginary parts, so each A-fragment load of a warp is one coalesced 256-byte read (L2 / L1).
 // The gathered input columns X (and the low-rank intermediate T) are B operands in shared memory,
-// planar re / im, column-major with a leading dimension = 4 (mod 16) (conflict-free fragments).
+// double2 (re, im) column-major with a leading dimension = 4 (mod 8) double2 (conflict-free
+// 128-bit fragment loads).  X is gathered with cp.async into a double buffer: the next chunk's
+// columns are in flight while the current chunk computes.
 #define GT_T 128
 #define GT_CT 2   // 8-column tiles per warp unit (GT_P: pair columns per chunk, 16 or 32)
 
@@ -296,42 +298,59 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 11) / 16) * 16 + 4; }  // >= k, = 4 mod 16
+__host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 + 4; }  // >= k, = 4 mod 8
 
-// One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem planes).
-// mode 0: write C into the smem planes Tr/Ti (ldt); mode 1: Y[sOut[col]*s_out + row] += C (plain RMW);
-// mode 2: same with atomics.
+// One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem double2).
+// mode 0: write C into the smem tile Ts (ldt); mode 1: Y[sOut[col]*s_out + row] += C (plain RMW, the
+// Y values are loaded before the k loop so their latency overlaps the MMAs); mode 2: same with atomics.
 template <int GT_P, int MODE>
-__device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, const double* Br,
-                                         const double* Bi, int ldb, double* Tr, double* Ti, int ldt,
-                                         double2* __restrict__ Y, const int* sOut, int s_out, int nb) {
+__device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, const double2* Bs, int ldb,
+                                         double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut, int s_out,
+                                         int nb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int CG = GT_P / 8 / GT_CT;
   const int nunits = Mt * CG;
   const int g = lane >> 2, t = lane & 3;
   for (int u = warp; u < nunits; u += GT_T / 32) {
     const int mt = u / CG, cg = u - mt * CG;
+    const int row = mt * 8 + g;
+    double2 yv[GT_CT][2];
+    if (MODE == 1) {
+#pragma unroll
+      for (int c = 0; c < GT_CT; ++c)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int col = (cg * GT_CT + c) * 8 + 2 * t + i;
+          yv[c][i] = (row < s_out && col < nb) ? Y[(int64_t)sOut[col] * s_out + row] : make_double2(0.0, 0.0);
+        }
+    }
     double acc[GT_CT][3][2];
 #pragma unroll
     for (int c = 0; c < GT_CT; ++c)
 #pragma unroll
       for (int q = 0; q < 3; ++q) acc[c][q][0] = acc[c][q][1] = 0.0;
     const double* ap = Ag + (size_t)mt * Kt * 64 + lane;
-    const int boff = (cg * GT_CT * 8 + g) * ldb + t;
+    const double2* bp = Bs + (cg * GT_CT * 8 + g) * ldb + t;
 #pragma unroll 4
     for (int kt = 0; kt < Kt; ++kt) {
       const double ar = __ldg(ap + kt * 64), ai = __ldg(ap + kt * 64 + 32);
       const double as = ar + ai;
 #pragma unroll
       for (int c = 0; c < GT_CT; ++c) {
-        const double br = Br[boff + c * 8 * ldb + kt * 4], bi = Bi[boff + c * 8 * ldb + kt * 4];
-        dmma(acc[c][0][0], acc[c][0][1], ar, br);
-        dmma(acc[c][1][0], acc[c][1][1], ai, bi);
-        dmma(acc[c][2][0], acc[c][2][1], as, br + bi);
+        const double2 b = bp[c * 8 * ldb + kt * 4];
+        dmma(acc[c][0][0], acc[c][0][1], ar, b.x);
+        dmma(acc[c][1][0], acc[c][1][1], ai, b.y);
+        dmma(acc[c][2][0], acc[c][2][1], as, b.x + b.y);
       }
     }
-    const int row = mt * 8 + g;
 #pragma unroll
     for (int c = 0; c < GT_CT; ++c)
 #pragma unroll
@@ -340,18 +359,14 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         const double re = acc[c][0][i] - acc[c][1][i];
         const double im = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
         if (MODE == 0) {
-          Tr[col * ldt + row] = re;
-          Ti[col * ldt + row] = im;
+          Ts[col * ldt + row] = make_double2(re, im);
         } else if (row < s_out && col < nb) {
           double2* y = Y + (int64_t)sOut[col] * s_out + row;
           if (MODE == 2) {
             atomicAdd(&y->x, re);
             atomicAdd(&y->y, im);
           } else {
-            double2 v = *y;
-            v.x += re;
-            v.y += im;
-            *y = v;
+            *y = make_double2(yv[c][i].x + re, yv[c][i].y + im);
           }
         }
       }
@@ -360,61 +375,88 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
 
 template <int GT_P>
 __global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
-  extern __shared__ double gsm[];
+  extern __shared__ double2 gsm2[];
   const int s_in = T.s_in, s_out = T.s_out;
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
-  double* Xr = gsm;
-  double* Xi = Xr + GT_P * ldx;
-  double* Tr = Xi + GT_P * ldx;
-  double* Ti = Tr + GT_P * ldt;
-  __shared__ int sOut[GT_P];
+  double2* Ts = gsm2 + 2 * GT_P * ldx;
+  __shared__ int sOut[2][GT_P], sIn[2][GT_P];
   const int tid = threadIdx.x;
   const int64_t item = T.item_order[blockIdx.x];
-  const int kp = kin * 4;
-  for (int64_t e = T.item_ptr[item]; e < T.item_ptr[item + 1]; ++e) {
+  const int64_t e_end = T.item_ptr[item + 1];
+  // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
+  for (int i = tid; i < 2 * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
+  // chunk cursor (entry e, first pair c0)
+  int64_t e = T.item_ptr[item], c0 = e < e_end ? T.ig_pb[e] : 0;
+  auto load_idx = [&](int buf, int64_t ee, int64_t cc) {
+    if (tid < GT_P) {
+      const int64_t p = cc + tid;
+      const bool v = p < T.ig_pe[ee];
+      sOut[buf][tid] = v ? T.out[p] : 0;
+      sIn[buf][tid] = v ? T.in[p] : -1;
+    }
+  };
+  auto issue_x = [&](int buf) {
+    for (int idx = tid; idx < GT_P * s_in; idx += GT_T) {
+      const int c = idx / s_in, k = idx - c * s_in;
+      const int src = sIn[buf][c];
+      if (src >= 0) cp_async16(gsm2 + buf * GT_P * ldx + c * ldx + k, &X[(int64_t)src * s_in + k]);
+    }
+    cp_async_commit();
+  };
+  if (e < e_end) load_idx(0, e, c0);
+  __syncthreads();
+  if (e < e_end) issue_x(0);
+  int buf = 0;
+  while (e < e_end) {
+    // next chunk
+    int64_t en = e, cn = c0 + GT_P;
+    if (cn >= T.ig_pe[en]) {
+      ++en;
+      cn = en < e_end ? T.ig_pb[en] : 0;
+    }
+    const bool has_next = en < e_end;
+    __syncthreads();  // chunk i-1 finished: buffer buf^1, T, indices of buf^1 are free
+    if (has_next) load_idx(buf ^ 1, en, cn);
+    __syncthreads();
+    if (has_next) {
+      issue_x(buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // X of this chunk visible
+    const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const double* Mg = T.pool + T.gmat[grp];
-    const int64_t pe = T.ig_pe[e];
-    for (int64_t c0 = T.ig_pb[e]; c0 < pe; c0 += GT_P) {
-      const int nb = (int)min((int64_t)GT_P, pe - c0);
+    if (rank >= 0) {
+      const int rt = (rank + 7) / 8;  // m tiles of V = k-tile pairs of U
+      gt_stage<GT_P, 0>(Mg, rt, kin, gsm2 + buf * GT_P * ldx, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
-      if (tid < GT_P) sOut[tid] = tid < nb ? T.out[c0 + tid] : 0;
-      for (int idx = tid; idx < GT_P * kp; idx += GT_T) {
-        const int c = idx / kp, k = idx - c * kp;
-        double2 v = make_double2(0.0, 0.0);
-        if (c < nb && k < s_in) v = X[(int64_t)T.in[c0 + c] * s_in + k];
-        Xr[c * ldx + k] = v.x;
-        Xi[c * ldx + k] = v.y;
-      }
-      __syncthreads();
-      if (rank >= 0) {
-        const int rt = (rank + 7) / 8;  // m tiles of V = k-tile pairs of U
-        gt_stage<GT_P, 0>(Mg, rt, kin, Xr, Xi, ldx, Tr, Ti, ldt, nullptr, nullptr, 0, 0);
-        __syncthreads();
-        const double* U = Mg + (size_t)rt * kin * 64;
-        if (T.atomic)
-          gt_stage<GT_P, 2>(U, mout, 2 * rt, Tr, Ti, ldt, nullptr, nullptr, 0, Y, sOut, s_out, nb);
-        else
-          gt_stage<GT_P, 1>(U, mout, 2 * rt, Tr, Ti, ldt, nullptr, nullptr, 0, Y, sOut, s_out, nb);
-      } else {
-        if (T.atomic)
-          gt_stage<GT_P, 2>(Mg, mout, kin, Xr, Xi, ldx, nullptr, nullptr, 0, Y, sOut, s_out, nb);
-        else
-          gt_stage<GT_P, 1>(Mg, mout, kin, Xr, Xi, ldx, nullptr, nullptr, 0, Y, sOut, s_out, nb);
-      }
+      const double* U = Mg + (size_t)rt * kin * 64;
+      if (T.atomic)
+        gt_stage<GT_P, 2>(U, mout, 2 * rt, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+      else
+        gt_stage<GT_P, 1>(U, mout, 2 * rt, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+    } else {
+      if (T.atomic)
+        gt_stage<GT_P, 2>(Mg, mout, kin, gsm2 + buf * GT_P * ldx, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+      else
+        gt_stage<GT_P, 1>(Mg, mout, kin, gsm2 + buf * GT_P * ldx, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
     }
+    e = en, c0 = cn, buf ^= 1;
   }
 }
 
 static size_t gt_smem_p(const GTrans& T, int p) {
   const int kin = (T.s_in + 3) / 4;
-  return (size_t)(2 * p * gt_ld(kin * 4) + 2 * p * gt_ld(T.rmax8)) * sizeof(double);
+  return (size_t)(2 * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2);
 }
 // 32 pair columns per chunk when the tiles are small, else 16 (>= 2 CTAs per SM)
 static int gt_cols(const GTrans& T) { return gt_smem_p(T, 32) <= 100 * 1024 ? 32 : 16; }
 size_t gtrans_smem(const GTrans& T) { return gt_smem_p(T, gt_cols(T)); }
+int gtrans_cols(const GTrans& T) { return gt_cols(T); }
 
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return;

@@ -55,6 +55,7 @@ struct GTrans {
 };
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
+int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)
 
 void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
                 const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha,

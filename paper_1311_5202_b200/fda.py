@@ -44,7 +44,7 @@ class fda_stats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in
                 ("n", "nleaves", "nlevels", "lmin", "p2p_leaf_pairs", "p2p_point_pairs", "m2l_pairs", "m2l_groups",
                  "m2l_lowrank_groups", "out_slots", "in_slots", "csr_nnz", "device_bytes", "owned_begin",
-                 "owned_end")] + \
+                 "owned_end", "owned_leaf_begin", "owned_leaf_end")] + \
                [(f, ctypes.c_double) for f in
                 ("setup_tree_s", "setup_lists_s", "setup_ops_s", "setup_upload_s", "flops_p2p", "flops_m2l",
                  "flops_m2m", "flops_l2l", "flops_s2m", "flops_l2t", "bytes_csr")]

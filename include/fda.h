@@ -69,10 +69,10 @@ typedef enum {
 /* Plan knobs (all optional; fda_options_default fills the defaults). */
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
-  double eps_internal;     /* truncation tolerance of every SVD / ID; 0 -> eps / 100 (R11) */
+  double eps_internal;     /* truncation tolerance of every SVD / ID; 0 -> eps / 30 (R11) */
   int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6) */
   int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths (default 8) */
-  double lf_p_switch;      /* w / lambda switch (default 0.5) */
+  double lf_p_switch;      /* w / lambda switch (default 0.75) */
   int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */
   int32_t single_leaf;     /* debug: no far field, every pair P2P (default 0) */
   int32_t hf_max_rows;     /* HF directional-set sample rows (default 6000) */

@@ -33,11 +33,11 @@ struct DevTrans {
 struct DevLeafOps {
   int level = 0, s = 0, nsurf = 0;
   int64_t nleaves = 0;       // all leaves of the level (S2M)
-  int64_t nleaves_own = 0;   // owned leaves (L2T) -- first nleaves_own of the l2t arrays
-  int32_t *leaf = nullptr, *slot = nullptr;
-  int32_t *leaf_own = nullptr, *slot_own = nullptr;
+  int64_t nleaves_own = 0;   // owned leaves (L2T)
+  int32_t *leaf = nullptr, *leaf_own = nullptr;
   double* surf = nullptr;
-  double2 *S = nullptr, *T = nullptr;
+  fda::GTrans s2m;           // H4 reduction: X[slot] += S chk[t]            (S = Sigma^-1 U^H, eq_cmps)
+  fda::GTrans l2t;           // H8 reduction: rho[t'] += T Y[slot]           (T = conj(U) Sigma^-1, eq_cmpt)
 };
 
 }  // namespace
@@ -71,6 +71,8 @@ struct fda_plan_s {
   std::vector<DevLevel> lv;
   std::vector<DevTrans> tr;
   std::vector<DevLeafOps> lo;
+  double2* surfbuf = nullptr;  // check potentials (S2M) / equivalent densities (L2T) of one level's leaves
+  int64_t surfbuf_n = 0;
   fda_stats st{};
   std::string logstr;
   int64_t last_launches = 0;  // kernels launched by the last apply
@@ -122,9 +124,6 @@ T* upload(fda_plan P, const std::vector<T>& v) {
 int32_t* upload_i32(fda_plan P, const std::vector<int64_t>& v) {
   std::vector<int32_t> t(v.begin(), v.end());
   return upload(P, t);
-}
-double2* upload_c(fda_plan P, const std::vector<cplx>& v) {
-  return upload(P, reinterpret_cast<const double2*>(v.data()), v.size());
 }
 
 // copy an input array (host or device) to a host vector
@@ -282,7 +281,11 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   std::vector<int32_t> order;
   for (int64_t i = 0; i < nitems; ++i)
     if (cnt[i + 1] > cnt[i]) order.push_back((int32_t)i);
-  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+  // Launch order: by (direction, Morton slab) so that concurrently resident items cover adjacent
+  // slabs and share their gathered X rows in L2 (FDA_ITEM_ORDER=cost: largest item first instead).
+  const char* io = getenv("FDA_ITEM_ORDER");
+  if (io && !strcmp(io, "cost"))
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
   T.n_items = (int64_t)order.size();
   T.item_order = upload(P, order);
   T.item_ptr = upload(P, iptr);
@@ -441,17 +444,38 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     DevLeafOps D;
     D.level = O.level, D.s = L.s, D.nsurf = L.nsurf;
     D.nleaves = (int64_t)O.leaf.size();
-    D.leaf = upload_i32(P, O.leaf), D.slot = upload_i32(P, O.slot);
+    D.leaf = upload_i32(P, O.leaf);
     std::vector<int64_t> lo_, so_;
     for (size_t t = 0; t < O.leaf.size(); ++t)
       if (O.leaf[t] >= P->leaf_b && O.leaf[t] < P->leaf_e) lo_.push_back(O.leaf[t]), so_.push_back(O.slot[t]);
     D.nleaves_own = (int64_t)lo_.size();
-    D.leaf_own = upload_i32(P, lo_), D.slot_own = upload_i32(P, so_);
+    D.leaf_own = upload_i32(P, lo_);
     std::vector<double> sf;
     for (const auto& p : L.ck_pts) sf.insert(sf.end(), {p[0], p[1], p[2]});
     D.surf = upload(P, sf);
-    D.S = upload_c(P, O.S);
-    D.T = upload_c(P, O.T);
+    {  // S2M reduction: pairs (out = leaf slot, in = leaf row t of the check-potential buffer)
+      GroupedPairs G;
+      G.out = O.slot;
+      G.in.resize(O.leaf.size());
+      for (size_t t = 0; t < O.leaf.size(); ++t) G.in[t] = (int64_t)t;
+      G.gptr.push_back((int64_t)G.out.size());
+      G.rank.push_back(-1);
+      G.mat.push_back(0);
+      D.s2m = make_items(P, G, L.out_cube, L.out_dir, (int64_t)L.cubes.size(), L.s, L.nsurf, O.S.data());
+    }
+    if (!lo_.empty()) {  // L2T reduction: pairs (out = owned leaf row t', in = leaf slot)
+      GroupedPairs G;
+      G.in = so_;
+      G.out.resize(lo_.size());
+      std::vector<int64_t> oc(lo_.size());
+      for (size_t t = 0; t < lo_.size(); ++t) G.out[t] = (int64_t)t, oc[t] = L.in_cube[so_[t]];
+      std::vector<int> od(lo_.size(), 0);
+      G.gptr.push_back((int64_t)G.out.size());
+      G.rank.push_back(-1);
+      G.mat.push_back(0);
+      D.l2t = make_items(P, G, oc, od, (int64_t)L.cubes.size(), L.nsurf, L.s, O.T.data());
+    }
+    P->surfbuf_n = std::max(P->surfbuf_n, (int64_t)O.leaf.size() * L.nsurf);
     for (int64_t t = 0; t < D.nleaves; ++t) {
       const double npt = (double)(lp[O.leaf[t] + 1] - lp[O.leaf[t]]);
       P->st.flops_s2m += npt * L.nsurf * 40.0 + 8.0 * L.s * L.nsurf;
@@ -462,6 +486,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     }
     P->lo.push_back(D);
   }
+  if (P->surfbuf_n) P->surfbuf = dalloc<double2>(P, (size_t)P->surfbuf_n);
   // stats
   fda_stats& s = P->st;
   s.n = n;
@@ -725,7 +750,8 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       for (auto& D : P->lv)
         if (D.n_out) ck(cudaMemsetAsync(D.X, 0, (size_t)D.n_out * D.s * sizeof(double2), st));
       for (const auto& O : P->lo) {
-        fda::launch_s2m(O.nleaves, O.leaf, O.slot, Lg, Pt, P->q, O.surf, O.nsurf, O.S, O.s, k, P->lv[O.level].X, st);
+        fda::launch_s2m_check(O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, P->surfbuf, st);
+        fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st);
         tr("s2m", O.level);
       }
     }
@@ -756,8 +782,10 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
     mark(7);
     if (far) {
       for (const auto& O : P->lo) {
-        fda::launch_l2t(O.nleaves_own, O.leaf_own, O.slot_own, Lg, Pt, O.surf, O.nsurf, O.T, O.s, k, alpha,
-                        P->lv[O.level].Y, P->outm, st);
+        if (!O.nleaves_own) continue;
+        ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
+        fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st);
+        fda::launch_l2t_eval(O.nleaves_own, O.leaf_own, Lg, Pt, O.surf, O.nsurf, k, alpha, P->surfbuf, P->outm, st);
         tr("l2t", O.level);
       }
     }
@@ -769,7 +797,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       int64_t L = 3;  // permute, p2p, unpermute
       if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
       if (far) {
-        for (const auto& O : P->lo) L += (O.nleaves > 0) + (O.nleaves_own > 0);
+        for (const auto& O : P->lo) L += 2 * (O.nleaves > 0) + 2 * (O.nleaves_own > 0);
         for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
         for (const auto& D : P->lv) L += D.m2l.n_items > 0;
       }

@@ -217,18 +217,18 @@ void launch_csr(int64_t r0, int64_t r1, const int64_t* rp, const int32_t* col, c
   k_csr<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(r0, r1, rp, col, val, phim, outm);
 }
 
-// ---------------------------------------------------------------- H4 S2M (dipole check potentials + reduction)
+// ---------------------------------------------------------------- H4 S2M (dipole check potentials)
+// chk[leaf][i] = sum_{j in leaf} dG/dn_y(a_i, y_j) q_j  on the leaf's outgoing check surface
+// (E_up of eq_evas2mh).  The reduction x~ = Sigma^-1 U^H chk (eq_cmps) is one
+// dense group of the grouped-translation kernel (all leaves of a level share S).
 #define S2M_T 128
-#define S2M_MAXC 4
-__global__ void __launch_bounds__(S2M_T) k_s2m(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ slots,
-                                               LeafGeom L, Points P, const double2* __restrict__ q,
-                                               const double* __restrict__ surf, int nsurf, const double2* __restrict__ S,
-                                               int s, double k, double2* __restrict__ X) {
-  extern __shared__ double2 chk[];  // nsurf
+#define S2M_MAXC 3
+__global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__ leaf_ids, LeafGeom L, Points P,
+                                                     const double2* __restrict__ q, const double* __restrict__ surf,
+                                                     int nsurf, double k, double2* __restrict__ chk) {
   __shared__ double sx[S2M_T], sy[S2M_T], sz[S2M_T], snx[S2M_T], sny[S2M_T], snz[S2M_T];
   __shared__ double2 sq[S2M_T];
   const int64_t leaf = leaf_ids[blockIdx.x];
-  const int64_t slot = slots[blockIdx.x];
   const int64_t pb = L.ptr[leaf], pe = L.ptr[leaf + 1];
   const double cx = L.cx[leaf], cy = L.cy[leaf], cz = L.cz[leaf];
   double ax[S2M_MAXC], ay[S2M_MAXC], az[S2M_MAXC];
@@ -258,23 +258,17 @@ __global__ void __launch_bounds__(S2M_T) k_s2m(const int32_t* __restrict__ leaf_
         cfma(acc[c], dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k), sq[u]);
     }
   }
+  double2* out = chk + (int64_t)blockIdx.x * nsurf;
 #pragma unroll
   for (int c = 0; c < S2M_MAXC; ++c) {
     const int i = threadIdx.x + c * S2M_T;
-    if (i < nsurf) chk[i] = acc[c];
-  }
-  __syncthreads();
-  for (int r = threadIdx.x; r < s; r += S2M_T) {
-    double2 x = make_double2(0.0, 0.0);
-    for (int i = 0; i < nsurf; ++i) cfma(x, S[r + (int64_t)i * s], chk[i]);
-    X[slot * s + r] = x;
+    if (i < nsurf) out[i] = acc[c];
   }
 }
-void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
-                const double2* q, const double* surf, int nsurf, const double2* S, int s, double k, double2* X,
-                cudaStream_t st) {
+void launch_s2m_check(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
+                      const double* surf, int nsurf, double k, double2* chk, cudaStream_t st) {
   if (nleaves <= 0) return;
-  k_s2m<<<(unsigned)nleaves, S2M_T, nsurf * sizeof(double2), st>>>(leaf_ids, slots, L, P, q, surf, nsurf, S, s, k, X);
+  k_s2m_check<<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
 }
 
 // ---------------------------------------------------------------- grouped translation (H5/H6/H7)
@@ -290,8 +284,10 @@ void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, 
 // double2 (re, im) column-major with a leading dimension = 4 (mod 8) double2 (conflict-free
 // 128-bit fragment loads).  X is gathered with cp.async into a double buffer: the next chunk's
 // columns are in flight while the current chunk computes.
-#define GT_T 128
+#define GT_T 256
+#define GT_W (GT_T / 32)
 #define GT_CT 2   // 8-column tiles per warp unit (GT_P: pair columns per chunk, 16 or 32)
+#define GT_SMEM_BUDGET (112 * 1024)  // per CTA: two CTAs (16 warps) per SM
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -309,18 +305,23 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 + 4; }  // >= k, = 4 mod 8
 
 // One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem double2).
-// mode 0: write C into the smem tile Ts (ldt); mode 1: Y[sOut[col]*s_out + row] += C (plain RMW, the
-// Y values are loaded before the k loop so their latency overlaps the MMAs); mode 2: same with atomics.
+// Work units (row tile, column group, k split) are spread over the CTA's warps.
+// mode 0: C += into the smem tile Ts (ldt) -- split over ksplit k ranges, combined with shared-memory
+//         atomics when ksplit > 1 (Ts zeroed by the caller);
+// mode 1: Y[sOut[col]*s_out + row] += C (plain RMW; Y loaded before the k loop so the load latency
+//         overlaps the MMAs); mode 2: same with global atomics.
 template <int GT_P, int MODE>
-__device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, const double2* Bs, int ldb,
-                                         double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut, int s_out,
-                                         int nb) {
+__device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
+                                         int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
+                                         int s_out, int nb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int CG = GT_P / 8 / GT_CT;
-  const int nunits = Mt * CG;
+  const int nunits = Mt * CG * ksplit;
   const int g = lane >> 2, t = lane & 3;
-  for (int u = warp; u < nunits; u += GT_T / 32) {
-    const int mt = u / CG, cg = u - mt * CG;
+  for (int u = warp; u < nunits; u += GT_W) {
+    const int ks = u % ksplit, rest = u / ksplit;
+    const int mt = rest / CG, cg = rest - mt * CG;
+    const int kb = (ks * Kt) / ksplit, ke = ((ks + 1) * Kt) / ksplit;
     const int row = mt * 8 + g;
     double2 yv[GT_CT][2];
     if (MODE == 1) {
@@ -340,7 +341,7 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
     const double* ap = Ag + (size_t)mt * Kt * 64 + lane;
     const double2* bp = Bs + (cg * GT_CT * 8 + g) * ldb + t;
 #pragma unroll 4
-    for (int kt = 0; kt < Kt; ++kt) {
+    for (int kt = kb; kt < ke; ++kt) {
       const double ar = __ldg(ap + kt * 64), ai = __ldg(ap + kt * 64 + 32);
       const double as = ar + ai;
 #pragma unroll
@@ -359,7 +360,13 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         const double re = acc[c][0][i] - acc[c][1][i];
         const double im = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
         if (MODE == 0) {
-          Ts[col * ldt + row] = make_double2(re, im);
+          double2* tp = &Ts[col * ldt + row];
+          if (ksplit > 1) {
+            atomicAdd(&tp->x, re);
+            atomicAdd(&tp->y, im);
+          } else {
+            *tp = make_double2(re, im);
+          }
         } else if (row < s_out && col < nb) {
           double2* y = Y + (int64_t)sOut[col] * s_out + row;
           if (MODE == 2) {
@@ -373,20 +380,21 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
   }
 }
 
-template <int GT_P>
-__global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
+// one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
+// current chunk computes; NBUF = 1 (large s_in): gather, then compute.
+template <int GT_P, int NBUF>
+__global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
   const int s_in = T.s_in, s_out = T.s_out;
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
-  double2* Ts = gsm2 + 2 * GT_P * ldx;
-  __shared__ int sOut[2][GT_P], sIn[2][GT_P];
+  double2* Ts = gsm2 + NBUF * GT_P * ldx;
+  __shared__ int sOut[NBUF][GT_P], sIn[NBUF][GT_P];
   const int tid = threadIdx.x;
   const int64_t item = T.item_order[blockIdx.x];
   const int64_t e_end = T.item_ptr[item + 1];
   // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
-  for (int i = tid; i < 2 * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
-  // chunk cursor (entry e, first pair c0)
+  for (int i = tid; i < NBUF * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
   int64_t e = T.item_ptr[item], c0 = e < e_end ? T.ig_pb[e] : 0;
   auto load_idx = [&](int buf, int64_t ee, int64_t cc) {
     if (tid < GT_P) {
@@ -397,10 +405,11 @@ __global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __rest
     }
   };
   auto issue_x = [&](int buf) {
+    double2* xb = gsm2 + buf * GT_P * ldx;
     for (int idx = tid; idx < GT_P * s_in; idx += GT_T) {
       const int c = idx / s_in, k = idx - c * s_in;
       const int src = sIn[buf][c];
-      if (src >= 0) cp_async16(gsm2 + buf * GT_P * ldx + c * ldx + k, &X[(int64_t)src * s_in + k]);
+      if (src >= 0) cp_async16(xb + c * ldx + k, &X[(int64_t)src * s_in + k]);
     }
     cp_async_commit();
   };
@@ -409,17 +418,24 @@ __global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __rest
   if (e < e_end) issue_x(0);
   int buf = 0;
   while (e < e_end) {
-    // next chunk
     int64_t en = e, cn = c0 + GT_P;
     if (cn >= T.ig_pe[en]) {
       ++en;
       cn = en < e_end ? T.ig_pb[en] : 0;
     }
     const bool has_next = en < e_end;
-    __syncthreads();  // chunk i-1 finished: buffer buf^1, T, indices of buf^1 are free
-    if (has_next) load_idx(buf ^ 1, en, cn);
+    const int grp = T.ig_group[e];
+    const int rank = T.grank[grp];
+    const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
+    const int ks1 = rank >= 0 ? max(1, min(kin / 4, (GT_W + rt * (GT_P / 8 / GT_CT) - 1) / (rt * (GT_P / 8 / GT_CT)))) : 1;
+    if (NBUF == 2) {
+      __syncthreads();  // previous chunk finished: buffer buf^1, Ts, indices of buf^1 are free
+      if (has_next) load_idx(buf ^ 1, en, cn);
+    }
+    if (rank >= 0 && ks1 > 1)
+      for (int i = tid; i < GT_P * ldt; i += GT_T) Ts[i] = make_double2(0.0, 0.0);
     __syncthreads();
-    if (has_next) {
+    if (NBUF == 2 && has_next) {
       issue_x(buf ^ 1);
       cp_async_wait<1>();
     } else {
@@ -427,68 +443,93 @@ __global__ void __launch_bounds__(GT_T) k_gtrans(GTrans T, const double2* __rest
     }
     __syncthreads();  // X of this chunk visible
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
-    const int grp = T.ig_group[e];
-    const int rank = T.grank[grp];
     const double* Mg = T.pool + T.gmat[grp];
+    const double2* xb = gsm2 + buf * GT_P * ldx;
     if (rank >= 0) {
-      const int rt = (rank + 7) / 8;  // m tiles of V = k-tile pairs of U
-      gt_stage<GT_P, 0>(Mg, rt, kin, gsm2 + buf * GT_P * ldx, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      gt_stage<GT_P, 0>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
       const double* U = Mg + (size_t)rt * kin * 64;
       if (T.atomic)
-        gt_stage<GT_P, 2>(U, mout, 2 * rt, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
       else
-        gt_stage<GT_P, 1>(U, mout, 2 * rt, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
     } else {
       if (T.atomic)
-        gt_stage<GT_P, 2>(Mg, mout, kin, gsm2 + buf * GT_P * ldx, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
       else
-        gt_stage<GT_P, 1>(Mg, mout, kin, gsm2 + buf * GT_P * ldx, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
     }
-    e = en, c0 = cn, buf ^= 1;
+    if (NBUF == 1 && has_next) {
+      __syncthreads();  // chunk finished: X buffer and indices are free
+      load_idx(0, en, cn);
+      __syncthreads();
+      issue_x(0);
+    }
+    e = en, c0 = cn;
+    if (NBUF == 2) buf ^= 1;
   }
 }
 
-static size_t gt_smem_p(const GTrans& T, int p) {
+static size_t gt_smem(const GTrans& T, int p, int nbuf) {
   const int kin = (T.s_in + 3) / 4;
-  return (size_t)(2 * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2);
+  return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2);
 }
-// 32 pair columns per chunk when the tiles are small, else 16 (>= 2 CTAs per SM)
-static int gt_cols(const GTrans& T) { return gt_smem_p(T, 32) <= 100 * 1024 ? 32 : 16; }
-size_t gtrans_smem(const GTrans& T) { return gt_smem_p(T, gt_cols(T)); }
-int gtrans_cols(const GTrans& T) { return gt_cols(T); }
+// chunk width and buffering: the widest that keeps two CTAs per SM
+static void gt_cfg(const GTrans& T, int* p, int* nbuf) {
+  const int cand[4][2] = {{32, 2}, {32, 1}, {16, 2}, {16, 1}};
+  for (auto& c : cand)
+    if (gt_smem(T, c[0], c[1]) <= GT_SMEM_BUDGET) {
+      *p = c[0], *nbuf = c[1];
+      return;
+    }
+  *p = 16, *nbuf = 1;
+}
+size_t gtrans_smem(const GTrans& T) {
+  int p, nb;
+  gt_cfg(T, &p, &nb);
+  return gt_smem(T, p, nb);
+}
+int gtrans_cols(const GTrans& T) {
+  int p, nb;
+  gt_cfg(T, &p, &nb);
+  return p;
+}
+
+template <int P, int NB>
+static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<P, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_gtrans<P, NB><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+}
 
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return;
-  const int p = gt_cols(T);
-  const size_t sm = gt_smem_p(T, p);
-  if (p == 32) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_gtrans<32><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
-  } else {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_gtrans<16><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
-  }
+  int p, nb;
+  gt_cfg(T, &p, &nb);
+  const size_t sm = gt_smem(T, p, nb);
+  if (p == 32 && nb == 2) gt_launch<32, 2>(T, X, Y, sm, st);
+  else if (p == 32) gt_launch<32, 1>(T, X, Y, sm, st);
+  else if (nb == 2) gt_launch<16, 2>(T, X, Y, sm, st);
+  else gt_launch<16, 1>(T, X, Y, sm, st);
 }
 
 // ---------------------------------------------------------------- H8 L2T
+// out_i += sum_b [G(x_i, b) + alpha dG/dn_x(x_i, b)] rho[leaf][b] over the leaf's incoming equivalent
+// surface (E_dn of eq_eval2t).  rho = conj(U) Sigma^-1 y~ (eq_cmpt) comes from the
+// grouped-translation kernel.
 #define L2T_T 128
-__global__ void __launch_bounds__(L2T_T) k_l2t(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ slots,
-                                               LeafGeom L, Points P, const double* __restrict__ surf, int nsurf,
-                                               const double2* __restrict__ T, int s, double k, double2 alpha,
-                                               const double2* __restrict__ Y, double2* __restrict__ outm) {
-  extern __shared__ double2 rho[];  // nsurf
+__global__ void __launch_bounds__(L2T_T) k_l2t_eval(const int32_t* __restrict__ leaf_ids, LeafGeom L, Points P,
+                                                    const double* __restrict__ surf, int nsurf, double k,
+                                                    double2 alpha, const double2* __restrict__ rhoall,
+                                                    double2* __restrict__ outm) {
+  extern __shared__ double2 rho[];  // nsurf (+ 3 nsurf doubles of surface points)
+  double* sp = reinterpret_cast<double*>(rho + nsurf);
   __shared__ double2 red[L2T_T];
   const int64_t leaf = leaf_ids[blockIdx.x];
-  const int64_t slot = slots[blockIdx.x];
   const int64_t pb = L.ptr[leaf], pe = L.ptr[leaf + 1];
   const double cx = L.cx[leaf], cy = L.cy[leaf], cz = L.cz[leaf];
-  const double2* y = Y + slot * s;
-  for (int i = threadIdx.x; i < nsurf; i += L2T_T) {
-    double2 v = make_double2(0.0, 0.0);
-    for (int r = 0; r < s; ++r) cfma(v, T[i + (int64_t)r * nsurf], y[r]);
-    rho[i] = v;
-  }
+  const double2* rl = rhoall + (int64_t)blockIdx.x * nsurf;
+  for (int i = threadIdx.x; i < nsurf; i += L2T_T) rho[i] = rl[i];
+  for (int i = threadIdx.x; i < 3 * nsurf; i += L2T_T) sp[i] = surf[i];
   __syncthreads();
   const int nt = (int)(pe - pb);
   const int ntp = nt >= L2T_T ? L2T_T : next_pow2(nt);
@@ -502,7 +543,7 @@ __global__ void __launch_bounds__(L2T_T) k_l2t(const int32_t* __restrict__ leaf_
       const double xi = P.x[i] - cx, yi = P.y[i] - cy, zi = P.z[i] - cz;
       const double nxi = P.nx[i], nyi = P.ny[i], nzi = P.nz[i];
       for (int b = my_sl; b < nsurf; b += nsl)
-        cfma(acc, bm_g(xi - surf[3 * b], yi - surf[3 * b + 1], zi - surf[3 * b + 2], nxi, nyi, nzi, k, alpha), rho[b]);
+        cfma(acc, bm_g(xi - sp[3 * b], yi - sp[3 * b + 1], zi - sp[3 * b + 2], nxi, nyi, nzi, k, alpha), rho[b]);
     }
     red[threadIdx.x] = acc;
     __syncthreads();
@@ -514,12 +555,11 @@ __global__ void __launch_bounds__(L2T_T) k_l2t(const int32_t* __restrict__ leaf_
     __syncthreads();
   }
 }
-void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
-                const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha, const double2* Y,
-                double2* outm, cudaStream_t st) {
+void launch_l2t_eval(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double* surf, int nsurf,
+                     double k, double2 alpha, const double2* rho, double2* outm, cudaStream_t st) {
   if (nleaves <= 0) return;
-  k_l2t<<<(unsigned)nleaves, L2T_T, nsurf * sizeof(double2), st>>>(leaf_ids, slots, L, P, surf, nsurf, T, s, k, alpha,
-                                                                   Y, outm);
+  k_l2t_eval<<<(unsigned)nleaves, L2T_T, nsurf * (sizeof(double2) + 3 * sizeof(double)), st>>>(
+      leaf_ids, L, P, surf, nsurf, k, alpha, rho, outm);
 }
 
 }  // namespace fda

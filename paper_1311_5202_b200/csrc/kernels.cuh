@@ -29,9 +29,12 @@ void launch_p2p(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, 
                 cudaStream_t st);
 void launch_csr(int64_t row_begin, int64_t row_end, const int64_t* rp, const int32_t* col, const double2* val,
                 const double2* phim, double2* outm, cudaStream_t st);
-void launch_s2m(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
-                const double2* q, const double* surf /* nsurf x 3, relative */, int nsurf, const double2* S,
-                int s, double k, double2* X, cudaStream_t st);
+// H4: dipole check potentials chk[t][i] of leaf leaf_ids[t] on its check surface (nsurf points, relative)
+void launch_s2m_check(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
+                      const double* surf, int nsurf, double k, double2* chk, cudaStream_t st);
+// H8: out += E_dn rho over the leaves' equivalent surfaces; rho[t][b] for leaf leaf_ids[t]
+void launch_l2t_eval(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double* surf, int nsurf,
+                     double k, double2 alpha, const double2* rho, double2* outm, cudaStream_t st);
 // Grouped translation (H5 M2M, H6 M2L, H7 L2L): one CTA per work item; an item owns a
 // disjoint set of output slots and walks a list of groups, each group = one matrix
 // (dense s_out x s_in, or low-rank U (s_out x r) V (r x s_in)) applied to its pairs:
@@ -56,9 +59,5 @@ struct GTrans {
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
 int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)
-
-void launch_l2t(int64_t nleaves, const int32_t* leaf_ids, const int32_t* slots, LeafGeom L, Points P,
-                const double* surf, int nsurf, const double2* T, int s, double k, double2 alpha,
-                const double2* Y, double2* outm, cudaStream_t st);
 
 }  // namespace fda

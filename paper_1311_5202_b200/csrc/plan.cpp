@@ -134,7 +134,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   P.alpha = alpha;
   P.eps = eps;
   P.opt = opt;
-  P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
+  P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 30.0;  // DESIGN.md R11 (calibrated at config 5)
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
   P.np = opt.np > 0 ? opt.np : (int)std::max(30.0, std::round(50.0 * (-std::log10(eps) - 3.0)));
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;

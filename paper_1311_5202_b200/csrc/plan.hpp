@@ -22,10 +22,10 @@ namespace fda {
 
 struct Options {
   int np = 0;               // leaf threshold N_p; 0 -> from eps (eq_npleaf, sign-corrected)
-  double eps_int = 0;       // internal truncation tolerance; 0 -> eps / 100 (R11)
+  double eps_int = 0;       // internal truncation tolerance; 0 -> eps / 30 (R11)
   int lf_p_low = 6;         // LF surface points per edge for w/lambda < lf_p_switch
   int lf_p_high = 8;        // ... for w/lambda >= lf_p_switch
-  double lf_p_switch = 0.5;
+  double lf_p_switch = 0.75;
   int lowrank = 1;          // low-rank M2L (eq_lrdk) on/off
   int single_leaf = 0;      // debug: no far field, root is the only leaf (everything P2P)
   int max_depth = 20;

@@ -214,15 +214,19 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   // parallelism first (>= 8 items per SM), then ~2 chunks of pairs per (item, group) where the groups allow
   int64_t S = std::max<int64_t>((int64_t)(ppg / (2 * cols)), (8 * 148 + nd - 1) / nd);
   S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
-  if (ppg / (double)S < 0.75 * cols) {
+  // FDA_GT_MODE=atomic|owned forces the item kind (experiments); FDA_GT_CHUNK: pairs per atomic item
+  const char* gm = getenv("FDA_GT_MODE");
+  const int64_t chunk = getenv("FDA_GT_CHUNK") ? std::max(1, atoi(getenv("FDA_GT_CHUNK"))) : 128;
+  const bool force_atomic = gm && !strcmp(gm, "atomic"), force_owned = gm && !strcmp(gm, "owned");
+  if (force_atomic || (!force_owned && ppg / (double)S < 0.75 * cols)) {
     // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items
     // (chunks of <= 128 pairs of one group) reuse the matrix; outputs then need atomics.
     std::vector<int64_t> iptr{0}, igpb, igpe;
     std::vector<int32_t> igg, order;
     std::vector<double> cost;
     for (int64_t g = 0; g < ng; ++g)
-      for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; p += 128) {
-        const int64_t q = std::min<int64_t>(p + 128, G.gptr[g + 1]);
+      for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; p += chunk) {
+        const int64_t q = std::min<int64_t>(p + chunk, G.gptr[g + 1]);
         igg.push_back((int32_t)g), igpb.push_back(p), igpe.push_back(q);
         iptr.push_back((int64_t)igg.size());
         const int r = G.rank[g];
@@ -281,10 +285,10 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   std::vector<int32_t> order;
   for (int64_t i = 0; i < nitems; ++i)
     if (cnt[i + 1] > cnt[i]) order.push_back((int32_t)i);
-  // Launch order: by (direction, Morton slab) so that concurrently resident items cover adjacent
-  // slabs and share their gathered X rows in L2 (FDA_ITEM_ORDER=cost: largest item first instead).
+  // Launch order: largest item first (measured at config 5: 10-30% faster per M2L level than the
+  // (direction, Morton slab) order, profiles/r01_m2l_order.md; FDA_ITEM_ORDER=morton selects the latter).
   const char* io = getenv("FDA_ITEM_ORDER");
-  if (io && !strcmp(io, "cost"))
+  if (!(io && !strcmp(io, "morton")))
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
   T.n_items = (int64_t)order.size();
   T.item_order = upload(P, order);

@@ -1,6 +1,8 @@
 // kernels.cu -- device kernels of the FDA Burton-Miller apply.  See kernels.cuh.
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace fda {
 
 #define FDA_INV4PI 0.079577471545947667884
@@ -231,38 +233,40 @@ __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__
   const int64_t leaf = leaf_ids[blockIdx.x];
   const int64_t pb = L.ptr[leaf], pe = L.ptr[leaf + 1];
   const double cx = L.cx[leaf], cy = L.cy[leaf], cz = L.cz[leaf];
-  double ax[S2M_MAXC], ay[S2M_MAXC], az[S2M_MAXC];
-  double2 acc[S2M_MAXC];
-#pragma unroll
-  for (int c = 0; c < S2M_MAXC; ++c) {
-    const int i = threadIdx.x + c * S2M_T;
-    acc[c] = make_double2(0.0, 0.0);
-    ax[c] = ay[c] = az[c] = 0.0;
-    if (i < nsurf) ax[c] = cx + surf[3 * i], ay[c] = cy + surf[3 * i + 1], az[c] = cz + surf[3 * i + 2];
-  }
-  for (int64_t s0 = pb; s0 < pe; s0 += S2M_T) {
-    const int64_t j = s0 + threadIdx.x;
-    __syncthreads();
-    if (j < pe) {
-      sx[threadIdx.x] = P.x[j], sy[threadIdx.x] = P.y[j], sz[threadIdx.x] = P.z[j];
-      snx[threadIdx.x] = P.nx[j], sny[threadIdx.x] = P.ny[j], snz[threadIdx.x] = P.nz[j];
-      sq[threadIdx.x] = q[j];
-    }
-    __syncthreads();
-    const int cnt = (int)min((int64_t)S2M_T, pe - s0);
+  double2* out = chk + (int64_t)blockIdx.x * nsurf;
+  for (int i0 = 0; i0 < nsurf; i0 += S2M_T * S2M_MAXC) {  // check-point blocks (one pass for nsurf <= 384)
+    double ax[S2M_MAXC], ay[S2M_MAXC], az[S2M_MAXC];
+    double2 acc[S2M_MAXC];
 #pragma unroll
     for (int c = 0; c < S2M_MAXC; ++c) {
-      const int i = threadIdx.x + c * S2M_T;
-      if (i >= nsurf) break;
-      for (int u = 0; u < cnt; ++u)
-        cfma(acc[c], dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k), sq[u]);
+      const int i = i0 + threadIdx.x + c * S2M_T;
+      acc[c] = make_double2(0.0, 0.0);
+      ax[c] = ay[c] = az[c] = 0.0;
+      if (i < nsurf) ax[c] = cx + surf[3 * i], ay[c] = cy + surf[3 * i + 1], az[c] = cz + surf[3 * i + 2];
     }
-  }
-  double2* out = chk + (int64_t)blockIdx.x * nsurf;
+    for (int64_t s0 = pb; s0 < pe; s0 += S2M_T) {
+      const int64_t j = s0 + threadIdx.x;
+      __syncthreads();
+      if (j < pe) {
+        sx[threadIdx.x] = P.x[j], sy[threadIdx.x] = P.y[j], sz[threadIdx.x] = P.z[j];
+        snx[threadIdx.x] = P.nx[j], sny[threadIdx.x] = P.ny[j], snz[threadIdx.x] = P.nz[j];
+        sq[threadIdx.x] = q[j];
+      }
+      __syncthreads();
+      const int cnt = (int)min((int64_t)S2M_T, pe - s0);
 #pragma unroll
-  for (int c = 0; c < S2M_MAXC; ++c) {
-    const int i = threadIdx.x + c * S2M_T;
-    if (i < nsurf) out[i] = acc[c];
+      for (int c = 0; c < S2M_MAXC; ++c) {
+        const int i = i0 + threadIdx.x + c * S2M_T;
+        if (i >= nsurf) break;
+        for (int u = 0; u < cnt; ++u)
+          cfma(acc[c], dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k), sq[u]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < S2M_MAXC; ++c) {
+      const int i = i0 + threadIdx.x + c * S2M_T;
+      if (i < nsurf) out[i] = acc[c];
+    }
   }
 }
 void launch_s2m_check(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,

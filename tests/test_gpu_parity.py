@@ -139,14 +139,16 @@ def test_host_pointers_and_linearity(cfg1):
         fda.fda_plan_destroy(h)
 
 
-@pytest.mark.parametrize("name,nu,k", [("hf-small", 16, 50.0), ("lf-small", 16, 2.0)])
-def test_full_apply_full_oracle(name, nu, k):
+@pytest.mark.parametrize("name,nu,k,opts", [("hf-small", 16, 50.0, {}), ("lf-small", 16, 2.0, {}),
+                                           # p = 10: 488 surface points (> one check-point block of k_s2m_check)
+                                           ("lf-p10", 16, 2.0, {"lf_p_low": 10, "lf_p_high": 10})])
+def test_full_apply_full_oracle(name, nu, k, opts):
     fda = _fda()
     p = synth.make_problem("x", k=k, nu=nu)
     csr = p.correction(seed=3)
     phi = synth.random_phi(p.N, 5)
     ref = oracle.apply_rows(p.x, p.n, p.w, p.k, p.alpha, phi, csr=csr)
-    h = _plan(p, verbose=1)
+    h = _plan(p, verbose=1, **opts)
     try:
         fda.fda_plan_set_correction(h, _dev(csr[0]), _dev(csr[1]), _dev(csr[2].view(np.float64)))
         got = _run(h, phi)

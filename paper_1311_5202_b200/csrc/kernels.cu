@@ -290,7 +290,9 @@ void launch_s2m_check(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Poin
 // columns are in flight while the current chunk computes.
 #define GT_T 256
 #define GT_W (GT_T / 32)
-#define GT_CT 2   // 8-column tiles per warp unit (GT_P: pair columns per chunk, 16 or 32)
+// A warp unit computes (8 rows) x (CT 8-column tiles); CT = GT_P/8 (all the chunk's columns: each A
+// fragment feeds 3*CT DMMAs) for the T stage and the atomic output, CT = 2 for owned outputs (more
+// units -> better balance across warps when the output has few row tiles).
 #define GT_SMEM_BUDGET (112 * 1024)  // per CTA: two CTAs (16 warps) per SM
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -314,7 +316,7 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 //         atomics when ksplit > 1 (Ts zeroed by the caller);
 // mode 1: Y[sOut[col]*s_out + row] += C (plain RMW; Y loaded before the k loop so the load latency
 //         overlaps the MMAs); mode 2: same with global atomics.
-template <int GT_P, int MODE>
+template <int GT_P, int MODE, int GT_CT>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
                                          int s_out, int nb) {
@@ -384,6 +386,15 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
   }
 }
 
+// k split of a stage with units = Mt row tiles (all columns): enough units for every warp, units a
+// multiple of the warp count when possible, at least 3 k tiles per split.
+__device__ __forceinline__ int gt_ksplit(int Mt, int Kt) {
+  if (Mt >= 2 * GT_W) return 1;
+  int ks = (GT_W + Mt - 1) / Mt;
+  while ((Mt * ks) % GT_W && ks < 2 * GT_W) ++ks;
+  return max(1, min(ks, Kt / 3));
+}
+
 // one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
 // current chunk computes; NBUF = 1 (large s_in): gather, then compute.
 template <int GT_P, int NBUF>
@@ -431,7 +442,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
-    const int ks1 = rank >= 0 ? max(1, min(kin / 4, (GT_W + rt * (GT_P / 8 / GT_CT) - 1) / (rt * (GT_P / 8 / GT_CT)))) : 1;
+    const int ks1 = rank >= 0 ? gt_ksplit(rt, kin) : 1;
     if (NBUF == 2) {
       __syncthreads();  // previous chunk finished: buffer buf^1, Ts, indices of buf^1 are free
       if (has_next) load_idx(buf ^ 1, en, cn);
@@ -450,18 +461,20 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const double* Mg = T.pool + T.gmat[grp];
     const double2* xb = gsm2 + buf * GT_P * ldx;
     if (rank >= 0) {
-      gt_stage<GT_P, 0>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      gt_stage<GT_P, 0, GT_P / 8>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
       const double* U = Mg + (size_t)rt * kin * 64;
       if (T.atomic)
-        gt_stage<GT_P, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 2, GT_P / 8>(U, mout, 2 * rt, gt_ksplit(mout, 2 * rt), Ts, ldt, nullptr, 0, Y, sOut[buf],
+                                    s_out, nb);
       else
-        gt_stage<GT_P, 1>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
     } else {
       if (T.atomic)
-        gt_stage<GT_P, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 2, GT_P / 8>(Mg, mout, kin, gt_ksplit(mout, kin), xb, ldx, nullptr, 0, Y, sOut[buf], s_out,
+                                    nb);
       else
-        gt_stage<GT_P, 1>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
     }
     if (NBUF == 1 && has_next) {
       __syncthreads();  // chunk finished: X buffer and indices are free

@@ -69,7 +69,7 @@ typedef enum {
 /* Plan knobs (all optional; fda_options_default fills the defaults). */
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
-  double eps_internal;     /* truncation tolerance of every SVD / ID; 0 -> eps / 30 (R11) */
+  double eps_internal;     /* expansion truncation (R+ SVDs, HF interpolative selection); 0 -> eps / 100 (R11) */
   int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6) */
   int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths (default 8) */
   double lf_p_switch;      /* w / lambda switch (default 0.75) */
@@ -79,6 +79,7 @@ typedef struct {
   double hf_spacing;       /* HF candidate spacing in wavelengths (default 0.25) */
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1) */
   int32_t verbose;         /* plan log (fda_plan_log) */
+  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
   int32_t host_only;       /* diagnostics: build the host plan only (tree, lists, operators), no device;
                               fda_apply* then returns FDA_ERR_STATE.  Lets CPU tests audit the lists. */
 } fda_options;

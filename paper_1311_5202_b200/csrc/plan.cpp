@@ -134,7 +134,10 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   P.alpha = alpha;
   P.eps = eps;
   P.opt = opt;
-  P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 30.0;  // DESIGN.md R11 (calibrated at config 5)
+  // DESIGN.md R11 / R23: expansion truncation (R+, HF interpolative selection) at eps_int, low-rank M2L
+  // truncation at eps_lr (measured: the low-rank cut contributes no visible error at eps_int)
+  P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
+  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 3.0;
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
   P.np = opt.np > 0 ? opt.np : (int)std::max(30.0, std::round(50.0 * (-std::log10(eps) - 3.0)));
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;
@@ -747,11 +750,11 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       std::vector<cplx>& out = gm[g];
       if (opt.lowrank && Kt.m > 1) {
         Mat Q, Rq;
-        std::vector<int64_t> piv = pivoted_qr(Kt, 0.1 * eps_int, Kt.n, &Q, &Rq);
+        std::vector<int64_t> piv = pivoted_qr(Kt, 0.1 * P.eps_lr, Kt.n, &Q, &Rq);
         SVD sv = svd_truncated(Rq, 0.0);
         int r = 0;
         for (double v : sv.s)
-          if (v >= eps_int * sv.s[0]) ++r;
+          if (v >= P.eps_lr * sv.s[0]) ++r;
         if (2 * r < std::max(Kt.m, Kt.n)) {
           rank = r;
           // U^ = Q U_R S (s x r), V^ = V_R^H (r x s), padded to the level size

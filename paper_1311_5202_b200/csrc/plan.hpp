@@ -22,7 +22,8 @@ namespace fda {
 
 struct Options {
   int np = 0;               // leaf threshold N_p; 0 -> from eps (eq_npleaf, sign-corrected)
-  double eps_int = 0;       // internal truncation tolerance; 0 -> eps / 30 (R11)
+  double eps_int = 0;       // expansion truncation tolerance; 0 -> eps / 100 (R11)
+  double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps / 3 (R23)
   int lf_p_low = 6;         // LF surface points per edge for w/lambda < lf_p_switch
   int lf_p_high = 8;        // ... for w/lambda >= lf_p_switch
   double lf_p_switch = 0.75;
@@ -90,7 +91,7 @@ struct HostPlan {
   int64_t n = 0;
   double k = 0;
   std::complex<double> alpha;
-  double eps = 1e-4, eps_int = 1e-5;
+  double eps = 1e-4, eps_int = 1e-5, eps_lr = 1e-5;
   int np = 50;
   Options opt;
   std::vector<double> px, py, pz, nx, ny, nz, w;

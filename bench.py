@@ -122,7 +122,7 @@ def run_reference(args, rank, world):
     cores = oracle.num_threads()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS.get(args.config, args.config), "N": p.N, "k": p.k, "eps": p.eps,
                        "rows_per_step": nrow},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",

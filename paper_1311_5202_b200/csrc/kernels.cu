@@ -386,13 +386,18 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
   }
 }
 
-// k split of a stage with units = Mt row tiles (all columns): enough units for every warp, units a
-// multiple of the warp count when possible, at least 3 k tiles per split.
-__device__ __forceinline__ int gt_ksplit(int Mt, int Kt) {
+// k split of a stage with units = Mt row tiles (all columns).  T stage (shared-memory atomics, cheap):
+// enough units for every warp, a multiple of the warp count when possible; Y stage (global atomics,
+// each split adds its partial sums): the fewest splits that give every warp a unit.  >= 3 k tiles each.
+__device__ __forceinline__ int gt_ksplit_t(int Mt, int Kt) {
   if (Mt >= 2 * GT_W) return 1;
   int ks = (GT_W + Mt - 1) / Mt;
   while ((Mt * ks) % GT_W && ks < 2 * GT_W) ++ks;
   return max(1, min(ks, Kt / 3));
+}
+__device__ __forceinline__ int gt_ksplit_y(int Mt, int Kt) {
+  if (Mt >= GT_W) return 1;
+  return max(1, min((GT_W + Mt - 1) / Mt, Kt / 3));
 }
 
 // one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
@@ -404,34 +409,34 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
   double2* Ts = gsm2 + NBUF * GT_P * ldx;
-  __shared__ int sOut[NBUF][GT_P], sIn[NBUF][GT_P];
+  __shared__ int sOut[2][GT_P], sIn[2][GT_P];  // pair indices: current / next chunk
   const int tid = threadIdx.x;
   const int64_t item = T.item_order[blockIdx.x];
   const int64_t e_end = T.item_ptr[item + 1];
   // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
   for (int i = tid; i < NBUF * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
   int64_t e = T.item_ptr[item], c0 = e < e_end ? T.ig_pb[e] : 0;
-  auto load_idx = [&](int buf, int64_t ee, int64_t cc) {
+  auto load_idx = [&](int ib, int64_t ee, int64_t cc) {
     if (tid < GT_P) {
       const int64_t p = cc + tid;
       const bool v = p < T.ig_pe[ee];
-      sOut[buf][tid] = v ? T.out[p] : 0;
-      sIn[buf][tid] = v ? T.in[p] : -1;
+      sOut[ib][tid] = v ? T.out[p] : 0;
+      sIn[ib][tid] = v ? T.in[p] : -1;
     }
   };
-  auto issue_x = [&](int buf) {
-    double2* xb = gsm2 + buf * GT_P * ldx;
+  auto issue_x = [&](int xbuf, int ib) {
+    double2* xb = gsm2 + xbuf * GT_P * ldx;
     for (int idx = tid; idx < GT_P * s_in; idx += GT_T) {
       const int c = idx / s_in, k = idx - c * s_in;
-      const int src = sIn[buf][c];
+      const int src = sIn[ib][c];
       if (src >= 0) cp_async16(xb + c * ldx + k, &X[(int64_t)src * s_in + k]);
     }
     cp_async_commit();
   };
   if (e < e_end) load_idx(0, e, c0);
   __syncthreads();
-  if (e < e_end) issue_x(0);
-  int buf = 0;
+  if (e < e_end) issue_x(0, 0);
+  int xbuf = 0, ib = 0;
   while (e < e_end) {
     int64_t en = e, cn = c0 + GT_P;
     if (cn >= T.ig_pe[en]) {
@@ -442,16 +447,14 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
-    const int ks1 = rank >= 0 ? gt_ksplit(rt, kin) : 1;
-    if (NBUF == 2) {
-      __syncthreads();  // previous chunk finished: buffer buf^1, Ts, indices of buf^1 are free
-      if (has_next) load_idx(buf ^ 1, en, cn);
-    }
+    const int ks1 = rank >= 0 ? gt_ksplit_t(rt, kin) : 1;
+    __syncthreads();  // previous chunk finished: Ts, indices ib^1 (and X buffer xbuf^1) are free
+    if (has_next) load_idx(ib ^ 1, en, cn);
     if (rank >= 0 && ks1 > 1)
       for (int i = tid; i < GT_P * ldt; i += GT_T) Ts[i] = make_double2(0.0, 0.0);
     __syncthreads();
     if (NBUF == 2 && has_next) {
-      issue_x(buf ^ 1);
+      issue_x(xbuf ^ 1, ib ^ 1);  // next chunk's columns stream in while this chunk computes
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -459,31 +462,31 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     __syncthreads();  // X of this chunk visible
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
     const double* Mg = T.pool + T.gmat[grp];
-    const double2* xb = gsm2 + buf * GT_P * ldx;
+    const double2* xb = gsm2 + xbuf * GT_P * ldx;
     if (rank >= 0) {
       gt_stage<GT_P, 0, GT_P / 8>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
+      // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
+      if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);
       const double* U = Mg + (size_t)rt * kin * 64;
       if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8>(U, mout, 2 * rt, gt_ksplit(mout, 2 * rt), Ts, ldt, nullptr, 0, Y, sOut[buf],
+        gt_stage<GT_P, 2, GT_P / 8>(U, mout, 2 * rt, gt_ksplit_y(mout, 2 * rt), Ts, ldt, nullptr, 0, Y, sOut[ib],
                                     s_out, nb);
       else
-        gt_stage<GT_P, 1, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb);
     } else {
       if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8>(Mg, mout, kin, gt_ksplit(mout, kin), xb, ldx, nullptr, 0, Y, sOut[buf], s_out,
+        gt_stage<GT_P, 2, GT_P / 8>(Mg, mout, kin, gt_ksplit_y(mout, kin), xb, ldx, nullptr, 0, Y, sOut[ib], s_out,
                                     nb);
       else
-        gt_stage<GT_P, 1, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[buf], s_out, nb);
+        gt_stage<GT_P, 1, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
+      if (NBUF == 1 && has_next) {
+        __syncthreads();  // X buffer free
+        issue_x(0, ib ^ 1);
+      }
     }
-    if (NBUF == 1 && has_next) {
-      __syncthreads();  // chunk finished: X buffer and indices are free
-      load_idx(0, en, cn);
-      __syncthreads();
-      issue_x(0);
-    }
-    e = en, c0 = cn;
-    if (NBUF == 2) buf ^= 1;
+    e = en, c0 = cn, ib ^= 1;
+    if (NBUF == 2) xbuf ^= 1;
   }
 }
 

@@ -264,16 +264,24 @@ def main():
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
-    if dom == "csr":
-        ach = st["bytes_csr"] / (per[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
-                "traffic": traffic, "kernel": dom, "peak_source": pk_kind}
-    else:
-        peak, peak_src = fp64_peak_tflops(pk.get("sm_max_mhz", 1965.0))
-        ach = flops.get(dom, 0.0) / (per[dom] * 1e-3) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": traffic, "kernel": dom,
+    peak64, peak_src = fp64_peak_tflops(pk.get("sm_max_mhz", 1965.0))
+    # bound of each phase: the translations run on the FP64 tensor pipe (DMMA), P2P / surface
+    # evaluations on the FP64 ALU (sincos, rsqrt, DFMA), the correction SpMV on HBM
+    bound = {"m2l": "tensor", "m2m": "tensor", "l2l": "tensor", "p2p": "alu", "s2m": "alu", "l2t": "alu"}
+
+    def phase_roof(ph):
+        if ph == "csr":
+            a = st["bytes_csr"] / (per[ph] * 1e-3) / 1e9
+            return {"bound": "hbm", "achieved": a, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": a / pk["hbm_gbs"],
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}
+        a = flops.get(ph, 0.0) / (per[ph] * 1e-3) / 1e12
+        return {"bound": bound.get(ph, "alu"), "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
                 "peak_source": peak_src}
+
+    roof = dict(phase_roof(dom), traffic=traffic, kernel=dom)
+    roof_phases = {ph: {k_: (round(v, 4) if isinstance(v, float) else v) for k_, v in phase_roof(ph).items()
+                        if k_ in ("bound", "achieved", "frac")}
+                   for ph in ("p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t") if per.get(ph, 0) > 0}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -284,7 +292,8 @@ def main():
                            "l2": "inputs larger than L2 (correction CSR %.1f GB)" % (st["csr_nnz"] * 20 / 1e9)},
                 "e2e": {"value": N / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(N * 16),
                         "d2h_bytes_per_step": int(N * 16)},
-                "gpu_launches": None, "roofline": roof, "cpu_baseline": cpu_baseline, "clocks": clk,
+                "gpu_launches": None, "roofline": roof, "roofline_phases": roof_phases,
+                "cpu_baseline": cpu_baseline, "clocks": clk,
                 "phases_ms": {k_: round(v, 4) for k_, v in per.items()}, "parity": parity,
                 "setup_s": {"inputs": round(t_gen, 2), "plan": round(t_plan, 2), "tree": st["setup_tree_s"],
                             "lists": st["setup_lists_s"], "ops": st["setup_ops_s"], "upload": st["setup_upload_s"]},

@@ -30,7 +30,12 @@ def main():
     seq = ["permute", "p2p", "csr"] + ["s2m"] * (2 * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
           ["l2t"] * (2 * nlf) + ["unpermute"]
     out = {}
-    for ph, i in zip(seq, order[start:start + len(seq)]):
+    # consecutive applies launch the same sequence: read it cyclically from the first k_permute_scale
+    # (the capture must hold at least one apply's worth of launches)
+    n = len(seq)
+    assert len(order) >= n, "capture shorter than one apply"
+    base = [order[start + j] if start + j < len(order) else order[start + j - n] for j in range(n)]
+    for ph, i in zip(seq, base):
         d = per[i]
         b = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
         out[ph] = out.get(ph, 0.0) + b

@@ -175,10 +175,12 @@ inline int pad4(int v) { return (v + 3) / 4 * 4; }
 // Fragment-order pool of the groups' matrices.  raw: the plan's column-major pool; a dense group is
 // s_out x s_in (ld s_out) at G.mat[g]; a low-rank group is U (s_out x r, ld s_out) then V (r x s_in, ld r).
 // Rewrites G.mat to offsets (doubles) into the returned pool.
-std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s_in, int* rmax8) {
+std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s_in, int* rmax8, int64_t* mmax) {
   std::vector<double> pool;
   *rmax8 = 0;
+  *mmax = 0;
   for (size_t g = 0; g < G.rank.size(); ++g) {
+    const size_t before = pool.size();
     const cplx* A = raw + G.mat[g];
     const int r = G.rank[g];
     G.mat[g] = (int64_t)pool.size();
@@ -190,6 +192,7 @@ std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s
       frag_append(pool, s_out, r, pad8(s_out), pad8(r), [&](int i, int j) { return A[i + (int64_t)j * s_out]; });
       *rmax8 = std::max(*rmax8, pad8(r));
     }
+    *mmax = std::max<int64_t>(*mmax, (int64_t)(pool.size() - before));
   }
   return pool;
 }
@@ -201,7 +204,9 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   if (np == 0) return T;
   {
     int rmax8 = 0;
-    std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8);
+    int64_t mmax = 0;
+    std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8, &mmax);
+    T.mmax = mmax;
     T.pool = upload(P, pool);
     T.rmax8 = rmax8;
     T.s_out = s_out, T.s_in = s_in;

@@ -316,7 +316,7 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 //         atomics when ksplit > 1 (Ts zeroed by the caller);
 // mode 1: Y[sOut[col]*s_out + row] += C (plain RMW; Y loaded before the k loop so the load latency
 //         overlaps the MMAs); mode 2: same with global atomics.
-template <int GT_P, int MODE, int GT_CT>
+template <int GT_P, int MODE, int GT_CT, bool ASM = false>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
                                          int s_out, int nb) {
@@ -348,7 +348,7 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
     const double2* bp = Bs + (cg * GT_CT * 8 + g) * ldb + t;
 #pragma unroll 4
     for (int kt = kb; kt < ke; ++kt) {
-      const double ar = __ldg(ap + kt * 64), ai = __ldg(ap + kt * 64 + 32);
+      const double ar = ASM ? ap[kt * 64] : __ldg(ap + kt * 64), ai = ASM ? ap[kt * 64 + 32] : __ldg(ap + kt * 64 + 32);
       const double as = ar + ai;
 #pragma unroll
       for (int c = 0; c < GT_CT; ++c) {
@@ -402,13 +402,17 @@ __device__ __forceinline__ int gt_ksplit_y(int Mt, int Kt) {
 
 // one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
 // current chunk computes; NBUF = 1 (large s_in): gather, then compute.
-template <int GT_P, int NBUF>
+template <int GT_P, int NBUF, bool STAGE>
 __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
   const int s_in = T.s_in, s_out = T.s_out;
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
   double2* Ts = gsm2 + NBUF * GT_P * ldx;
+  // STAGE: the current group's fragment-order matrix block is copied (cp.async, contiguous) into shared
+  // memory once per group and read from there by every chunk of the item
+  double* Ms = reinterpret_cast<double*>(Ts + GT_P * ldt);
+  int staged = -1;
   __shared__ int sOut[2][GT_P], sIn[2][GT_P];  // pair indices: current / next chunk
   const int tid = threadIdx.x;
   const int64_t item = T.item_order[blockIdx.x];
@@ -452,6 +456,13 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     if (has_next) load_idx(ib ^ 1, en, cn);
     if (rank >= 0 && ks1 > 1)
       for (int i = tid; i < GT_P * ldt; i += GT_T) Ts[i] = make_double2(0.0, 0.0);
+    if (STAGE && grp != staged) {
+      const double* src = T.pool + T.gmat[grp];
+      const int nd = rank >= 0 ? (rt * kin + mout * 2 * rt) * 64 : mout * kin * 64;  // doubles, multiple of 64
+      for (int i = tid; i < nd / 2; i += GT_T) cp_async16(Ms + 2 * i, src + 2 * i);
+      cp_async_commit();
+      staged = grp;
+    }
     __syncthreads();
     if (NBUF == 2 && has_next) {
       issue_x(xbuf ^ 1, ib ^ 1);  // next chunk's columns stream in while this chunk computes
@@ -461,25 +472,25 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     }
     __syncthreads();  // X of this chunk visible
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
-    const double* Mg = T.pool + T.gmat[grp];
+    const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
     const double2* xb = gsm2 + xbuf * GT_P * ldx;
     if (rank >= 0) {
-      gt_stage<GT_P, 0, GT_P / 8>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      gt_stage<GT_P, 0, GT_P / 8, STAGE>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
       // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
       if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);
       const double* U = Mg + (size_t)rt * kin * 64;
       if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8>(U, mout, 2 * rt, gt_ksplit_y(mout, 2 * rt), Ts, ldt, nullptr, 0, Y, sOut[ib],
-                                    s_out, nb);
+        gt_stage<GT_P, 2, GT_P / 8, STAGE>(U, mout, 2 * rt, gt_ksplit_y(mout, 2 * rt), Ts, ldt, nullptr, 0, Y,
+                                           sOut[ib], s_out, nb);
       else
-        gt_stage<GT_P, 1, 2>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb);
+        gt_stage<GT_P, 1, 2, STAGE>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb);
     } else {
       if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8>(Mg, mout, kin, gt_ksplit_y(mout, kin), xb, ldx, nullptr, 0, Y, sOut[ib], s_out,
-                                    nb);
+        gt_stage<GT_P, 2, GT_P / 8, STAGE>(Mg, mout, kin, gt_ksplit_y(mout, kin), xb, ldx, nullptr, 0, Y, sOut[ib],
+                                           s_out, nb);
       else
-        gt_stage<GT_P, 1, 2>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
+        gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       if (NBUF == 1 && has_next) {
         __syncthreads();  // X buffer free
         issue_x(0, ib ^ 1);
@@ -490,46 +501,57 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   }
 }
 
-static size_t gt_smem(const GTrans& T, int p, int nbuf) {
+static size_t gt_smem(const GTrans& T, int p, int nbuf, bool stage) {
   const int kin = (T.s_in + 3) / 4;
-  return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2);
+  return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2) +
+         (stage ? (size_t)T.mmax * sizeof(double) : 0);
 }
-// chunk width and buffering: the widest that keeps two CTAs per SM
-static void gt_cfg(const GTrans& T, int* p, int* nbuf) {
-  const int cand[4][2] = {{32, 2}, {32, 1}, {16, 2}, {16, 1}};
-  for (auto& c : cand)
-    if (gt_smem(T, c[0], c[1]) <= GT_SMEM_BUDGET) {
-      *p = c[0], *nbuf = c[1];
+// chunk width, buffering and matrix staging: the first candidate that keeps two CTAs per SM
+// (FDA_GT_STAGE=0 disables staging)
+static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
+  static const bool allow = !(getenv("FDA_GT_STAGE") && getenv("FDA_GT_STAGE")[0] == '0');
+  const int cand[6][3] = {{32, 1, 1}, {32, 2, 0}, {32, 1, 0}, {16, 1, 1}, {16, 2, 0}, {16, 1, 0}};
+  for (auto& c : cand) {
+    if (c[2] && !allow) continue;
+    if (gt_smem(T, c[0], c[1], c[2]) <= GT_SMEM_BUDGET) {
+      *p = c[0], *nbuf = c[1], *stage = c[2];
       return;
     }
-  *p = 16, *nbuf = 1;
+  }
+  *p = 16, *nbuf = 1, *stage = false;
 }
 size_t gtrans_smem(const GTrans& T) {
   int p, nb;
-  gt_cfg(T, &p, &nb);
-  return gt_smem(T, p, nb);
+  bool stg;
+  gt_cfg(T, &p, &nb, &stg);
+  return gt_smem(T, p, nb, stg);
 }
 int gtrans_cols(const GTrans& T) {
   int p, nb;
-  gt_cfg(T, &p, &nb);
+  bool stg;
+  gt_cfg(T, &p, &nb, &stg);
   return p;
 }
 
-template <int P, int NB>
+template <int P, int NB, bool STG>
 static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans<P, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_gtrans<P, NB><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_gtrans<P, NB, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_gtrans<P, NB, STG><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
 }
 
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return;
   int p, nb;
-  gt_cfg(T, &p, &nb);
-  const size_t sm = gt_smem(T, p, nb);
-  if (p == 32 && nb == 2) gt_launch<32, 2>(T, X, Y, sm, st);
-  else if (p == 32) gt_launch<32, 1>(T, X, Y, sm, st);
-  else if (nb == 2) gt_launch<16, 2>(T, X, Y, sm, st);
-  else gt_launch<16, 1>(T, X, Y, sm, st);
+  bool stg;
+  gt_cfg(T, &p, &nb, &stg);
+  const size_t sm = gt_smem(T, p, nb, stg);
+  if (p == 32 && nb == 1 && stg) gt_launch<32, 1, true>(T, X, Y, sm, st);
+  else if (p == 32 && nb == 2) gt_launch<32, 2, false>(T, X, Y, sm, st);
+  else if (p == 32) gt_launch<32, 1, false>(T, X, Y, sm, st);
+  else if (stg) gt_launch<16, 1, true>(T, X, Y, sm, st);
+  else if (nb == 2) gt_launch<16, 2, false>(T, X, Y, sm, st);
+  else gt_launch<16, 1, false>(T, X, Y, sm, st);
 }
 
 // ---------------------------------------------------------------- H8 L2T

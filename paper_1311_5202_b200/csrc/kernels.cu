@@ -312,8 +312,7 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 
 // One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem double2).
 // Work units (row tile, column group, k split) are spread over the CTA's warps.
-// mode 0: C += into the smem tile Ts (ldt) -- split over ksplit k ranges, combined with shared-memory
-//         atomics when ksplit > 1 (Ts zeroed by the caller);
+// mode 0: C into the smem tile Ts (ldt) (ksplit must be 1: shared-memory FP64 atomics are CAS loops);
 // mode 1: Y[sOut[col]*s_out + row] += C (plain RMW; Y loaded before the k loop so the load latency
 //         overlaps the MMAs); mode 2: same with global atomics.
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
@@ -366,13 +365,7 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         const double re = acc[c][0][i] - acc[c][1][i];
         const double im = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
         if (MODE == 0) {
-          double2* tp = &Ts[col * ldt + row];
-          if (ksplit > 1) {
-            atomicAdd(&tp->x, re);
-            atomicAdd(&tp->y, im);
-          } else {
-            *tp = make_double2(re, im);
-          }
+          Ts[col * ldt + row] = make_double2(re, im);
         } else if (row < s_out && col < nb) {
           double2* y = Y + (int64_t)sOut[col] * s_out + row;
           if (MODE == 2) {
@@ -386,15 +379,8 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
   }
 }
 
-// k split of a stage with units = Mt row tiles (all columns).  T stage (shared-memory atomics, cheap):
-// enough units for every warp, a multiple of the warp count when possible; Y stage (global atomics,
-// each split adds its partial sums): the fewest splits that give every warp a unit.  >= 3 k tiles each.
-__device__ __forceinline__ int gt_ksplit_t(int Mt, int Kt) {
-  if (Mt >= 2 * GT_W) return 1;
-  int ks = (GT_W + Mt - 1) / Mt;
-  while ((Mt * ks) % GT_W && ks < 2 * GT_W) ++ks;
-  return max(1, min(ks, Kt / 3));
-}
+// k split of an atomic Y stage with units = Mt row tiles (all columns; each split adds its partial sums
+// with global atomics): the fewest splits that give every warp a unit, >= 3 k tiles each.
 __device__ __forceinline__ int gt_ksplit_y(int Mt, int Kt) {
   if (Mt >= GT_W) return 1;
   return max(1, min((GT_W + Mt - 1) / Mt, Kt / 3));
@@ -451,11 +437,11 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
-    const int ks1 = rank >= 0 ? gt_ksplit_t(rt, kin) : 1;
+    // T stage work units = (row tile, column tile(s)): no k split (shared-memory FP64 atomics are CAS
+    // loops on sm_100a); 2 column tiles per unit when that still gives half the warps a unit, else 1
+    const bool t_ct2 = rt * (GT_P / 16) >= GT_W / 2;
     __syncthreads();  // previous chunk finished: Ts, indices ib^1 (and X buffer xbuf^1) are free
     if (has_next) load_idx(ib ^ 1, en, cn);
-    if (rank >= 0 && ks1 > 1)
-      for (int i = tid; i < GT_P * ldt; i += GT_T) Ts[i] = make_double2(0.0, 0.0);
     if (STAGE && grp != staged) {
       const double* src = T.pool + T.gmat[grp];
       const int nd = rank >= 0 ? (rt * kin + mout * 2 * rt) * 64 : mout * kin * 64;  // doubles, multiple of 64
@@ -475,7 +461,10 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
     const double2* xb = gsm2 + xbuf * GT_P * ldx;
     if (rank >= 0) {
-      gt_stage<GT_P, 0, GT_P / 8, STAGE>(Mg, rt, kin, ks1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      if (t_ct2)
+        gt_stage<GT_P, 0, 2, STAGE>(Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      else
+        gt_stage<GT_P, 0, 1, STAGE>(Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
       // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
       if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);

@@ -318,7 +318,8 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
-                                         int s_out, int nb) {
+                                         int s_out, int nb, int lda_kt = 0) {
+  if (lda_kt == 0) lda_kt = Kt;  // k tiles per row tile in the fragment-order storage of A
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int CG = GT_P / 8 / GT_CT;
   const int nunits = Mt * CG * ksplit;
@@ -343,7 +344,7 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
     for (int c = 0; c < GT_CT; ++c)
 #pragma unroll
       for (int q = 0; q < 3; ++q) acc[c][q][0] = acc[c][q][1] = 0.0;
-    const double* ap = Ag + (size_t)mt * Kt * 64 + lane;
+    const double* ap = Ag + (size_t)mt * lda_kt * 64 + lane;
     const double2* bp = Bs + (cg * GT_CT * 8 + g) * ldb + t;
 #pragma unroll 4
     for (int kt = kb; kt < ke; ++kt) {
@@ -469,11 +470,13 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
       if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);
       const double* U = Mg + (size_t)rt * kin * 64;
+      // U is stored with pad8(r) columns; only ceil(r/4) k tiles are non-zero
+      const int kt2 = (rank + 3) / 4;
       if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8, STAGE>(U, mout, 2 * rt, gt_ksplit_y(mout, 2 * rt), Ts, ldt, nullptr, 0, Y,
-                                           sOut[ib], s_out, nb);
+        gt_stage<GT_P, 2, GT_P / 8, STAGE>(U, mout, kt2, gt_ksplit_y(mout, kt2), Ts, ldt, nullptr, 0, Y, sOut[ib],
+                                           s_out, nb, 2 * rt);
       else
-        gt_stage<GT_P, 1, 2, STAGE>(U, mout, 2 * rt, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb);
+        gt_stage<GT_P, 1, 2, STAGE>(U, mout, kt2, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
     } else {
       if (T.atomic)
         gt_stage<GT_P, 2, GT_P / 8, STAGE>(Mg, mout, kin, gt_ksplit_y(mout, kin), xb, ldx, nullptr, 0, Y, sOut[ib],

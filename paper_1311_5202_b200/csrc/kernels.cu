@@ -387,6 +387,33 @@ __device__ __forceinline__ int gt_ksplit_y(int Mt, int Kt) {
   return max(1, min((GT_W + Mt - 1) / Mt, Kt / 3));
 }
 
+// Column tiles per warp unit for a stage with Mt row tiles (x ksplit): the CT in {P/8, .., 2, 1} whose
+// unit count fills the warps best (ties -> the larger CT: each A fragment feeds more MMAs).
+template <int GT_P>
+__device__ __forceinline__ int gt_pick_ct(int Mt, int ks) {
+  int best = GT_P / 8;
+  double beff = -1.0;
+  for (int ct = GT_P / 8; ct >= 1; ct >>= 1) {
+    const int n = Mt * ks * (GT_P / 8 / ct);
+    const double eff = (double)n / (double)(GT_W * ((n + GT_W - 1) / GT_W));
+    if (eff > beff + 0.05) beff = eff, best = ct;
+  }
+  return best;
+}
+// dispatch a stage on a runtime CT
+template <int GT_P, int MODE, bool ASM>
+__device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ Ag, int Mt, int Kt, int ksplit,
+                                            const double2* Bs, int ldb, double2* Ts, int ldt,
+                                            double2* __restrict__ Y, const int* sOut, int s_out, int nb,
+                                            int lda_kt = 0) {
+  if (ct >= 4 && GT_P / 8 >= 4)
+    gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+  else if (ct >= 2)
+    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+  else
+    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+}
+
 // one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
 // current chunk computes; NBUF = 1 (large s_in): gather, then compute.
 template <int GT_P, int NBUF, bool STAGE>
@@ -438,9 +465,9 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
-    // T stage work units = (row tile, column tile(s)): no k split (shared-memory FP64 atomics are CAS
-    // loops on sm_100a); 2 column tiles per unit when that still gives half the warps a unit, else 1
-    const bool t_ct2 = rt * (GT_P / 16) >= GT_W / 2;
+    // T stage work units = (row tile, column tiles): no k split (shared-memory FP64 atomics are CAS
+    // loops on sm_100a); the column tiles per unit are chosen for warp balance
+    const int ct1 = rank >= 0 ? gt_pick_ct<GT_P>(rt, 1) : 1;
     __syncthreads();  // previous chunk finished: Ts, indices ib^1 (and X buffer xbuf^1) are free
     if (has_next) load_idx(ib ^ 1, en, cn);
     if (STAGE && grp != staged) {
@@ -462,26 +489,25 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
     const double2* xb = gsm2 + xbuf * GT_P * ldx;
     if (rank >= 0) {
-      if (t_ct2)
-        gt_stage<GT_P, 0, 2, STAGE>(Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
-      else
-        gt_stage<GT_P, 0, 1, STAGE>(Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();
       // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
       if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);
       const double* U = Mg + (size_t)rt * kin * 64;
       // U is stored with pad8(r) columns; only ceil(r/4) k tiles are non-zero
       const int kt2 = (rank + 3) / 4;
-      if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8, STAGE>(U, mout, kt2, gt_ksplit_y(mout, kt2), Ts, ldt, nullptr, 0, Y, sOut[ib],
-                                           s_out, nb, 2 * rt);
-      else
+      if (T.atomic) {
+        const int ks = gt_ksplit_y(mout, kt2);
+        gt_stage_ct<GT_P, 2, STAGE>(gt_pick_ct<GT_P>(mout, ks), U, mout, kt2, ks, Ts, ldt, nullptr, 0, Y, sOut[ib],
+                                    s_out, nb, 2 * rt);
+      } else
         gt_stage<GT_P, 1, 2, STAGE>(U, mout, kt2, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
     } else {
-      if (T.atomic)
-        gt_stage<GT_P, 2, GT_P / 8, STAGE>(Mg, mout, kin, gt_ksplit_y(mout, kin), xb, ldx, nullptr, 0, Y, sOut[ib],
-                                           s_out, nb);
-      else
+      if (T.atomic) {
+        const int ks = gt_ksplit_y(mout, kin);
+        gt_stage_ct<GT_P, 2, STAGE>(gt_pick_ct<GT_P>(mout, ks), Mg, mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib],
+                                    s_out, nb);
+      } else
         gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       if (NBUF == 1 && has_next) {
         __syncthreads();  // X buffer free

@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
     // T stage work units = (row tile, column tiles): no k split (shared-memory FP64 atomics are CAS
     // loops on sm_100a); the column tiles per unit are chosen for warp balance
-    const int ct1 = rank >= 0 ? gt_pick_ct<GT_P>(rt, 1) : 1;
+    int ct1 = T.ct1;  // > 0: forced (FDA_GT_CT1); 0: 2 column tiles when >= half the warps get a unit, else 1
+    if (ct1 <= 0) ct1 = rt * (GT_P / 16) >= GT_W / 2 ? 2 : 1;
     __syncthreads();  // previous chunk finished: Ts, indices ib^1 (and X buffer xbuf^1) are free
     if (has_next) load_idx(ib ^ 1, en, cn);
     if (STAGE && grp != staged) {
@@ -498,15 +499,15 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       const int kt2 = (rank + 3) / 4;
       if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kt2);
-        gt_stage_ct<GT_P, 2, STAGE>(gt_pick_ct<GT_P>(mout, ks), U, mout, kt2, ks, Ts, ldt, nullptr, 0, Y, sOut[ib],
-                                    s_out, nb, 2 * rt);
+        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), U, mout,
+                                    kt2, ks, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(U, mout, kt2, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
     } else {
       if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kin);
-        gt_stage_ct<GT_P, 2, STAGE>(gt_pick_ct<GT_P>(mout, ks), Mg, mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib],
-                                    s_out, nb);
+        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), Mg,
+                                    mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       if (NBUF == 1 && has_next) {

@@ -414,8 +414,10 @@ __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ A
     gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
 }
 
-// one CTA per work item; NBUF = 2: the next chunk's columns are gathered (cp.async) while the
-// current chunk computes; NBUF = 1 (large s_in): gather, then compute.
+// One CTA per work item.  Per chunk of GT_P pairs two barriers: [C] after the chunk's gather has
+// landed (cp.async), [D] between the low-rank stages.  The next chunk's gather is issued right after
+// [C] into the other buffer (NBUF = 2) or, with one buffer, after [D] (X is dead once T = V X) or
+// after the dense stage; pair indices are triple-buffered and fetched two chunks ahead.
 template <int GT_P, int NBUF, bool STAGE>
 __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
@@ -426,14 +428,20 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   // STAGE: the current group's fragment-order matrix block is copied (cp.async, contiguous) into shared
   // memory once per group and read from there by every chunk of the item
   double* Ms = reinterpret_cast<double*>(Ts + GT_P * ldt);
-  int staged = -1;
-  __shared__ int sOut[2][GT_P], sIn[2][GT_P];  // pair indices: current / next chunk
-  const int tid = threadIdx.x;
+  __shared__ int sOut[3][GT_P], sIn[3][GT_P];  // pair indices of chunks i, i+1, i+2 (mod 3)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t item = T.item_order[blockIdx.x];
-  const int64_t e_end = T.item_ptr[item + 1];
+  const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
+  if (e_beg >= e_end) return;
   // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
   for (int i = tid; i < NBUF * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
-  int64_t e = T.item_ptr[item], c0 = e < e_end ? T.ig_pb[e] : 0;
+  auto advance = [&](int64_t& ee, int64_t& cc) {
+    cc += GT_P;
+    if (cc >= T.ig_pe[ee]) {
+      ++ee;
+      cc = ee < e_end ? T.ig_pb[ee] : 0;
+    }
+  };
   auto load_idx = [&](int ib, int64_t ee, int64_t cc) {
     if (tid < GT_P) {
       const int64_t p = cc + tid;
@@ -442,61 +450,61 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       sIn[ib][tid] = v ? T.in[p] : -1;
     }
   };
-  auto issue_x = [&](int xbuf, int ib) {
+  auto issue_x = [&](int xbuf, int ib) {  // warp per pair column, lanes along k (no division)
     double2* xb = gsm2 + xbuf * GT_P * ldx;
-    for (int idx = tid; idx < GT_P * s_in; idx += GT_T) {
-      const int c = idx / s_in, k = idx - c * s_in;
+    for (int c = warp; c < GT_P; c += GT_W) {
       const int src = sIn[ib][c];
-      if (src >= 0) cp_async16(xb + c * ldx + k, &X[(int64_t)src * s_in + k]);
+      if (src < 0) continue;
+      const double2* xs = X + (int64_t)src * s_in;
+      for (int k = lane; k < s_in; k += 32) cp_async16(xb + c * ldx + k, xs + k);
     }
     cp_async_commit();
   };
-  if (e < e_end) load_idx(0, e, c0);
+  auto stage_m = [&](int grp) {
+    const int rank = T.grank[grp], rt = (rank + 7) / 8;
+    const double* src = T.pool + T.gmat[grp];
+    const int nd = rank >= 0 ? (rt * kin + mout * 2 * rt) * 64 : mout * kin * 64;  // doubles, multiple of 64
+    for (int i = tid; i < nd / 2; i += GT_T) cp_async16(Ms + 2 * i, src + 2 * i);
+    cp_async_commit();
+  };
+  // prologue: indices of chunks 0 and 1, matrix of chunk 0, gather of chunk 0
+  int64_t e = e_beg, c0 = T.ig_pb[e_beg];
+  int64_t e1 = e, c1 = c0;
+  advance(e1, c1);
+  load_idx(0, e, c0);
+  if (e1 < e_end) load_idx(1, e1, c1);
+  if (STAGE) stage_m(T.ig_group[e]);
   __syncthreads();
-  if (e < e_end) issue_x(0, 0);
+  issue_x(0, 0);
   int xbuf = 0, ib = 0;
   while (e < e_end) {
-    int64_t en = e, cn = c0 + GT_P;
-    if (cn >= T.ig_pe[en]) {
-      ++en;
-      cn = en < e_end ? T.ig_pb[en] : 0;
-    }
+    int64_t en = e, cn = c0;
+    advance(en, cn);
     const bool has_next = en < e_end;
+    int64_t e2 = en, c2 = cn;
+    if (has_next) advance(e2, c2);
+    const bool has_next2 = has_next && e2 < e_end;
+    const int ib1 = ib == 2 ? 0 : ib + 1, ib2 = ib1 == 2 ? 0 : ib1 + 1;
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
     const int rt = (rank + 7) / 8;  // low rank: m tiles of V = k-tile pairs of U
     // T stage work units = (row tile, column tiles): no k split (shared-memory FP64 atomics are CAS
-    // loops on sm_100a); the column tiles per unit are chosen for warp balance
-    int ct1 = T.ct1;  // > 0: forced (FDA_GT_CT1); 0: 2 column tiles when >= half the warps get a unit, else 1
+    // loops on sm_100a); 2 column tiles per unit when >= half the warps get a unit, else 1
+    int ct1 = T.ct1;
     if (ct1 <= 0) ct1 = rt * (GT_P / 16) >= GT_W / 2 ? 2 : 1;
-    __syncthreads();  // previous chunk finished: Ts, indices ib^1 (and X buffer xbuf^1) are free
-    if (has_next) load_idx(ib ^ 1, en, cn);
-    if (STAGE && grp != staged) {
-      const double* src = T.pool + T.gmat[grp];
-      const int nd = rank >= 0 ? (rt * kin + mout * 2 * rt) * 64 : mout * kin * 64;  // doubles, multiple of 64
-      for (int i = tid; i < nd / 2; i += GT_T) cp_async16(Ms + 2 * i, src + 2 * i);
-      cp_async_commit();
-      staged = grp;
-    }
-    __syncthreads();
-    if (NBUF == 2 && has_next) {
-      issue_x(xbuf ^ 1, ib ^ 1);  // next chunk's columns stream in while this chunk computes
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();  // X of this chunk visible
+    cp_async_wait<0>();
+    __syncthreads();  // [C] X (and Ms) of this chunk visible; previous chunk finished everywhere
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
     const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
     const double2* xb = gsm2 + xbuf * GT_P * ldx;
+    if (NBUF == 2 && has_next) issue_x(xbuf ^ 1, ib1);  // the other buffer was last read by chunk i-1
     if (rank >= 0) {
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
-      __syncthreads();
-      // single X buffer: X is dead after stage 1, so the next chunk's gather overlaps stage 2
-      if (NBUF == 1 && has_next) issue_x(0, ib ^ 1);
+      __syncthreads();  // [D] T complete, X of this chunk no longer read
+      if (NBUF == 1 && has_next) issue_x(0, ib1);
+      if (has_next2) load_idx(ib2, e2, c2);  // buffer ib2 held chunk i-1's indices (done at [C])
       const double* U = Mg + (size_t)rt * kin * 64;
-      // U is stored with pad8(r) columns; only ceil(r/4) k tiles are non-zero
-      const int kt2 = (rank + 3) / 4;
+      const int kt2 = (rank + 3) / 4;  // U is stored with pad8(r) columns; ceil(r/4) k tiles are non-zero
       if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kt2);
         gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), U, mout,
@@ -510,12 +518,17 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
                                     mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
+      if (has_next2) load_idx(ib2, e2, c2);
       if (NBUF == 1 && has_next) {
         __syncthreads();  // X buffer free
-        issue_x(0, ib ^ 1);
+        issue_x(0, ib1);
       }
     }
-    e = en, c0 = cn, ib ^= 1;
+    if (STAGE && has_next && T.ig_group[en] != grp) {
+      __syncthreads();  // every warp is done with Ms
+      stage_m(T.ig_group[en]);
+    }
+    e = en, c0 = cn, ib = ib1;
     if (NBUF == 2) xbuf ^= 1;
   }
 }

@@ -545,7 +545,9 @@ static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
   const int cand[6][3] = {{32, 1, 1}, {32, 2, 0}, {32, 1, 0}, {16, 1, 1}, {16, 2, 0}, {16, 1, 0}};
   for (auto& c : cand) {
     if (c[2] && !allow) continue;
-    if (gt_smem(T, c[0], c[1], c[2]) <= GT_SMEM_BUDGET) {
+    static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
+                                                           : (size_t)GT_SMEM_BUDGET;
+    if (gt_smem(T, c[0], c[1], c[2]) <= budget) {
       *p = c[0], *nbuf = c[1], *stage = c[2];
       return;
     }

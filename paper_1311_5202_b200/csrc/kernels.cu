@@ -1,6 +1,7 @@
 // kernels.cu -- device kernels of the FDA Burton-Miller apply.  See kernels.cuh.
 #include "kernels.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace fda {
@@ -430,22 +431,44 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   double* Ms = reinterpret_cast<double*>(Ts + GT_P * ldt);
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];  // pair indices of chunks i, i+1, i+2 (mod 3)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t item = T.item_order[blockIdx.x];
-  const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
-  if (e_beg >= e_end) return;
-  // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
-  for (int i = tid; i < NBUF * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
-  auto advance = [&](int64_t& ee, int64_t& cc) {
-    cc += GT_P;
-    if (cc >= T.ig_pe[ee]) {
-      ++ee;
-      cc = ee < e_end ? T.ig_pb[ee] : 0;
+  // Persistent CTAs: CTA b walks the items item_order[b], item_order[b + G], ... (G = gridDim.x) as one
+  // stream of chunks, so the next item's first gather overlaps the current item's last chunk and the
+  // items resident at any time stay the consecutive block of the launch order (Morton locality).
+  struct Cur {
+    int64_t j, e, e_end, c;  // item slot j, entry e in [item start, e_end), first pair c of the chunk
+  };
+  auto item_at = [&](Cur& u) {
+    while (u.j < T.n_items) {
+      const int64_t it = T.item_order[u.j];
+      u.e = T.item_ptr[it], u.e_end = T.item_ptr[it + 1];
+      if (u.e < u.e_end) {
+        u.c = T.ig_pb[u.e];
+        return;
+      }
+      u.j += gridDim.x;
     }
   };
-  auto load_idx = [&](int ib, int64_t ee, int64_t cc) {
+  auto valid = [&](const Cur& u) { return u.j < T.n_items; };
+  auto advance = [&](Cur& u) {
+    u.c += GT_P;
+    if (u.c >= T.ig_pe[u.e]) {
+      if (++u.e < u.e_end) {
+        u.c = T.ig_pb[u.e];
+      } else {
+        u.j += gridDim.x;
+        item_at(u);
+      }
+    }
+  };
+  Cur cur{(int64_t)blockIdx.x, 0, 0, 0};
+  item_at(cur);
+  if (!valid(cur)) return;
+  // zero the X buffers once: the padding rows k in [s_in, 4 kin) are never written by the gather
+  for (int i = tid; i < NBUF * GT_P * ldx; i += GT_T) gsm2[i] = make_double2(0.0, 0.0);
+  auto load_idx = [&](int ib, const Cur& u) {
     if (tid < GT_P) {
-      const int64_t p = cc + tid;
-      const bool v = p < T.ig_pe[ee];
+      const int64_t p = u.c + tid;
+      const bool v = p < T.ig_pe[u.e];
       sOut[ib][tid] = v ? T.out[p] : 0;
       sIn[ib][tid] = v ? T.in[p] : -1;
     }
@@ -468,22 +491,22 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     cp_async_commit();
   };
   // prologue: indices of chunks 0 and 1, matrix of chunk 0, gather of chunk 0
-  int64_t e = e_beg, c0 = T.ig_pb[e_beg];
-  int64_t e1 = e, c1 = c0;
-  advance(e1, c1);
-  load_idx(0, e, c0);
-  if (e1 < e_end) load_idx(1, e1, c1);
-  if (STAGE) stage_m(T.ig_group[e]);
+  Cur c1 = cur;
+  advance(c1);
+  load_idx(0, cur);
+  if (valid(c1)) load_idx(1, c1);
+  if (STAGE) stage_m(T.ig_group[cur.e]);
   __syncthreads();
   issue_x(0, 0);
   int xbuf = 0, ib = 0;
-  while (e < e_end) {
-    int64_t en = e, cn = c0;
-    advance(en, cn);
-    const bool has_next = en < e_end;
-    int64_t e2 = en, c2 = cn;
-    if (has_next) advance(e2, c2);
-    const bool has_next2 = has_next && e2 < e_end;
+  while (valid(cur)) {
+    Cur nx = cur;
+    advance(nx);
+    const bool has_next = valid(nx);
+    Cur n2 = nx;
+    if (has_next) advance(n2);
+    const bool has_next2 = has_next && valid(n2);
+    const int64_t e = cur.e, c0 = cur.c;
     const int ib1 = ib == 2 ? 0 : ib + 1, ib2 = ib1 == 2 ? 0 : ib1 + 1;
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp];
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
       __syncthreads();  // [D] T complete, X of this chunk no longer read
       if (NBUF == 1 && has_next) issue_x(0, ib1);
-      if (has_next2) load_idx(ib2, e2, c2);  // buffer ib2 held chunk i-1's indices (done at [C])
+      if (has_next2) load_idx(ib2, n2);  // buffer ib2 held chunk i-1's indices (done at [C])
       const double* U = Mg + (size_t)rt * kin * 64;
       const int kt2 = (rank + 3) / 4;  // U is stored with pad8(r) columns; ceil(r/4) k tiles are non-zero
       if (T.atomic) {
@@ -518,17 +541,17 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
                                     mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
-      if (has_next2) load_idx(ib2, e2, c2);
+      if (has_next2) load_idx(ib2, n2);
       if (NBUF == 1 && has_next) {
         __syncthreads();  // X buffer free
         issue_x(0, ib1);
       }
     }
-    if (STAGE && has_next && T.ig_group[en] != grp) {
+    if (STAGE && has_next && T.ig_group[nx.e] != grp) {
       __syncthreads();  // every warp is done with Ms
-      stage_m(T.ig_group[en]);
+      stage_m(T.ig_group[nx.e]);
     }
-    e = en, c0 = cn, ib = ib1;
+    cur = nx, ib = ib1;
     if (NBUF == 2) xbuf ^= 1;
   }
 }
@@ -571,7 +594,17 @@ template <int P, int NB, bool STG>
 static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024)
     cudaFuncSetAttribute(k_gtrans<P, NB, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_gtrans<P, NB, STG><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  // persistent: as many CTAs as fit at once (2 per SM at the default smem budget), at most one per item
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gtrans<P, NB, STG>, GT_T, sm);
+  const int64_t grid = std::min<int64_t>(T.n_items, (int64_t)std::max(1, per_sm) * nsm);
+  k_gtrans<P, NB, STG><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
 }
 
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {

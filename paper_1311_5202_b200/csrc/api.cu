@@ -226,7 +226,10 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   // Default: group-major items of <= 1024 pairs with atomic accumulation (measured at config 5: 400 ms
   // apply vs 440 ms with the automatic choice and 509 ms with owned items only; 1024 vs 256 pairs:
   // 332 vs 336 ms).
-  const int64_t chunk = getenv("FDA_GT_CHUNK") ? std::max(1, atoi(getenv("FDA_GT_CHUNK"))) : 1024;
+  // pairs per atomic item: up to 1024, but enough items to give every SM ~16 CTAs over the launch
+  const int64_t chunk = getenv("FDA_GT_CHUNK")
+                            ? std::max(1, atoi(getenv("FDA_GT_CHUNK")))
+                            : std::max<int64_t>(32, std::min<int64_t>(1024, (np / (16 * 148) + 31) / 32 * 32));
   const bool force_owned = gm && !strcmp(gm, "owned"), use_auto = gm && !strcmp(gm, "auto");
   if (!force_owned && (!use_auto || ppg / (double)S < 0.75 * cols)) {
     // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items

@@ -190,108 +190,10 @@ __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_
     __syncthreads();
   }
 }
-// P2P v2: one CTA per target leaf; all source points of the leaf's near list are staged in blocks of
-// up to P2P2_SB points (cp.async, source leaves located by a warp-parallel prefix sum + binary search),
-// so a typical leaf (~220 sources) needs one block; lanes = (target, source slice) as in k_p2p.
-#define P2P2_T 128
-#define P2P2_SB 512
-#define P2P2_ML 128
-__global__ void __launch_bounds__(P2P2_T) k_p2p2(const int64_t* __restrict__ leaf_ptr,
-                                                 const int64_t* __restrict__ p2p_ptr,
-                                                 const int32_t* __restrict__ p2p_src, Points P,
-                                                 const double2* __restrict__ q, double k, double2 alpha,
-                                                 double2* __restrict__ outm, int64_t leaf0) {
-  __shared__ double sx[P2P2_SB], sy[P2P2_SB], sz[P2P2_SB], snx[P2P2_SB], sny[P2P2_SB], snz[P2P2_SB];
-  __shared__ double2 sq[P2P2_SB];
-  __shared__ int sj[P2P2_SB];
-  __shared__ int lpre[P2P2_ML + 1];
-  __shared__ int64_t lbeg[P2P2_ML];
-  __shared__ double2 red[P2P2_T];
-  const int64_t t = leaf0 + blockIdx.x;
-  const int64_t tb = leaf_ptr[t], te = leaf_ptr[t + 1];
-  const int nt = (int)(te - tb);
-  const int ntp = nt >= P2P2_T ? P2P2_T : next_pow2(nt);
-  const int nsl = P2P2_T / ntp;
-  const int my_t = threadIdx.x % ntp, my_sl = threadIdx.x / ntp;
-  const int lane = threadIdx.x & 31;
-  const int64_t sb0 = p2p_ptr[t], se0 = p2p_ptr[t + 1];
-  for (int t0 = 0; t0 < nt; t0 += ntp) {
-    const int64_t i = tb + t0 + my_t;
-    const bool act = (t0 + my_t) < nt;
-    double xi = 0, yi = 0, zi = 0, nxi = 0, nyi = 0, nzi = 0;
-    if (act) xi = P.x[i], yi = P.y[i], zi = P.z[i], nxi = P.nx[i], nyi = P.ny[i], nzi = P.nz[i];
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t sb = sb0; sb < se0; sb += P2P2_ML) {
-      const int nl = (int)min((int64_t)P2P2_ML, se0 - sb);
-      __syncthreads();
-      if (threadIdx.x < 32) {  // warp 0: leaf sizes and their inclusive prefix sum
-        int carry = 0;
-        for (int l0 = 0; l0 < nl; l0 += 32) {
-          const int l = l0 + lane;
-          int cnt = 0;
-          if (l < nl) {
-            const int64_t sl = p2p_src[sb + l];
-            lbeg[l] = leaf_ptr[sl];
-            cnt = (int)(leaf_ptr[sl + 1] - leaf_ptr[sl]);
-          }
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, cnt, o);
-            if (lane >= o) cnt += v;
-          }
-          if (l < nl) lpre[l + 1] = carry + cnt;
-          carry += __shfl_sync(0xffffffffu, cnt, 31);
-        }
-        if (lane == 0) lpre[0] = 0;
-      }
-      __syncthreads();
-      const int tot = lpre[nl];
-      for (int s0 = 0; s0 < tot; s0 += P2P2_SB) {
-        const int cnt = min(P2P2_SB, tot - s0);
-        if (s0 > 0) __syncthreads();
-        for (int u = threadIdx.x; u < cnt; u += P2P2_T) {
-          const int jj = s0 + u;
-          int lo = 0, hi = nl - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (lpre[mid] <= jj) lo = mid;
-            else hi = mid - 1;
-          }
-          const int64_t j = lbeg[lo] + (jj - lpre[lo]);
-          sx[u] = P.x[j], sy[u] = P.y[j], sz[u] = P.z[j];
-          snx[u] = P.nx[j], sny[u] = P.ny[j], snz[u] = P.nz[j];
-          sq[u] = q[j];
-          sj[u] = (int)(j - tb);  // source index relative to the target leaf start (self test below)
-        }
-        __syncthreads();
-        if (act) {
-          const int me = t0 + my_t;
-          for (int u = my_sl; u < cnt; u += nsl) {
-            if (sj[u] == me) continue;
-            const double2 kv = bm_h(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha);
-            cfma(acc, kv, sq[u]);
-          }
-        }
-      }
-    }
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    if (my_sl == 0 && act) {
-      double2 s = red[my_t];
-      for (int sl = 1; sl < nsl; ++sl) s = cadd(s, red[my_t + sl * ntp]);
-      outm[i] = s;
-    }
-  }
-}
-
 void launch_p2p(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src, Points P,
                 const double2* q, double k, double2 alpha, double2* outm, int64_t leaf0, cudaStream_t st) {
   if (nleaf <= 0) return;
-  static const bool v1 = getenv("FDA_P2P") && !strcmp(getenv("FDA_P2P"), "v1");
-  if (v1) {
-    k_p2p<<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
-    return;
-  }
-  k_p2p2<<<(unsigned)nleaf, P2P2_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
+  k_p2p<<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
 }
 
 // ---------------------------------------------------------------- H3 correction SpMV (warp per row)

@@ -210,6 +210,8 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     T.pool = upload(P, pool);
     T.rmax8 = rmax8;
     T.s_out = s_out, T.s_in = s_in;
+    T.all_lowrank = 1;
+    for (int32_t r : G.rank) T.all_lowrank &= (r >= 0);
     if (getenv("FDA_GT_CT1")) T.ct1 = atoi(getenv("FDA_GT_CT1"));
     if (getenv("FDA_GT_CT2")) T.ct2 = atoi(getenv("FDA_GT_CT2"));
   }

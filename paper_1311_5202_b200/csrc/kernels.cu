@@ -320,13 +320,14 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
-                                         int s_out, int nb, int lda_kt = 0) {
+                                         int s_out, int nb, int lda_kt = 0, int wbase = 0, int nw = GT_W) {
   if (lda_kt == 0) lda_kt = Kt;  // k tiles per row tile in the fragment-order storage of A
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the units are spread over warps [wbase, wbase + nw) of the CTA
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbase;
   const int CG = GT_P / 8 / GT_CT;
   const int nunits = Mt * CG * ksplit;
   const int g = lane >> 2, t = lane & 3;
-  for (int u = warp; u < nunits; u += GT_W) {
+  for (int u = warp; u < nunits; u += nw) {
     const int ks = u % ksplit, rest = u / ksplit;
     const int mt = rest / CG, cg = rest - mt * CG;
     const int kb = (ks * Kt) / ksplit, ke = ((ks + 1) * Kt) / ksplit;
@@ -407,13 +408,14 @@ template <int GT_P, int MODE, bool ASM>
 __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ Ag, int Mt, int Kt, int ksplit,
                                             const double2* Bs, int ldb, double2* Ts, int ldt,
                                             double2* __restrict__ Y, const int* sOut, int s_out, int nb,
-                                            int lda_kt = 0) {
+                                            int lda_kt = 0, int wbase = 0, int nw = GT_W) {
   if (ct >= 4 && GT_P / 8 >= 4)
-    gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+    gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt,
+                                                      wbase, nw);
   else if (ct >= 2)
-    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
   else
-    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt);
+    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
 }
 
 // One CTA per work item.  Per chunk of GT_P pairs two barriers: [C] after the chunk's gather has
@@ -557,6 +559,117 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   }
 }
 
+// Warp-specialised variant for items whose groups are all low rank (atomic items): warps 0-3 run the
+// first stage T = V X of chunk i+1 while warps 4-7 run the second stage Y += U T of chunk i (T double
+// buffered), so neither stage's few work units leave half the CTA idle at a barrier.  One CTA
+// barrier per chunk; the stage-1 warps own the gather (cp.async) and wait for it with a named
+// barrier among themselves, overlapping the stage-2 warps' work.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+template <int GT_P, bool STAGE>
+__global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* __restrict__ X,
+                                                      double2* __restrict__ Y) {
+  extern __shared__ double2 gsm2[];
+  const int s_in = T.s_in, s_out = T.s_out;
+  const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;
+  const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
+  double2* Xs = gsm2;
+  double2* const T0 = gsm2 + GT_P * ldx;  // T double buffer: T0 (even chunks), T0 + GT_P ldt (odd)
+  double* Ms = reinterpret_cast<double*>(gsm2 + GT_P * ldx + 2 * GT_P * ldt);
+  __shared__ int sOut[3][GT_P], sIn[3][GT_P];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool grpA = warp < GT_W / 2;  // stage-1 warps (and the gather); the rest run stage 2
+  const int64_t item = T.item_order[blockIdx.x];
+  const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
+  if (e_beg >= e_end) return;
+  for (int i = tid; i < GT_P * ldx; i += GT_T) Xs[i] = make_double2(0.0, 0.0);
+  // chunk list of the item: entries (groups) e, pairs [c, c + GT_P)
+  auto advance = [&](int64_t& e, int64_t& c) {
+    c += GT_P;
+    if (c >= T.ig_pe[e]) {
+      ++e;
+      c = e < e_end ? T.ig_pb[e] : 0;
+    }
+  };
+  auto load_idx = [&](int ib, int64_t e, int64_t c) {  // by warp 0
+    if (tid < GT_P) {
+      const int64_t p = c + tid;
+      const bool v = p < T.ig_pe[e];
+      sOut[ib][tid] = v ? T.out[p] : 0;
+      sIn[ib][tid] = v ? T.in[p] : -1;
+    }
+  };
+  auto issue_x = [&](int ib) {  // by the stage-1 warps
+    for (int c = warp; c < GT_P; c += GT_W / 2) {
+      const int src = sIn[ib][c];
+      if (src < 0) continue;
+      const double2* xs = X + (int64_t)src * s_in;
+      for (int k = lane; k < s_in; k += 32) cp_async16(Xs + c * ldx + k, xs + k);
+    }
+    cp_async_commit();
+  };
+  // all groups of an atomic item are one group; stage its matrix once (all threads)
+  const int grp0 = T.ig_group[e_beg];
+  if (STAGE) {
+    const int rank = T.grank[grp0], rt = (rank + 7) / 8;
+    const double* src = T.pool + T.gmat[grp0];
+    const int nd = (rt * kin + mout * 2 * rt) * 64;
+    for (int i = tid; i < nd / 2; i += GT_T) cp_async16(Ms + 2 * i, src + 2 * i);
+    cp_async_commit();
+  }
+  int64_t ea = e_beg, ca = T.ig_pb[e_beg];  // chunk of the stage-1 warps (i)
+  int64_t e1 = ea, c1 = ca;
+  advance(e1, c1);
+  load_idx(0, ea, ca);
+  if (e1 < e_end) load_idx(1, e1, c1);
+  cp_async_wait<0>();
+  __syncthreads();
+  if (grpA) issue_x(0);
+  int64_t eb = -1, cb = 0;  // chunk of the stage-2 warps (i - 1); -1: none yet
+  int i = 0;
+  while (ea < e_end || eb >= 0) {
+    const int ia = i % 3, ibb = (i + 2) % 3;  // index buffers of chunks i and i - 1
+    if (grpA && ea < e_end) {
+      const int grp = T.ig_group[ea];
+      const int rank = T.grank[grp], rt = (rank + 7) / 8;
+      const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
+      cp_async_wait<0>();
+      named_bar(1, GT_T / 2);  // X of chunk i visible to the stage-1 warps
+      const int ct1 = (rt % 2 == 0) ? 2 : 1;  // units = rt x (4 / ct1): a multiple of the 4 stage-1 warps
+      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
+                                  0, 0, 0, GT_W / 2);
+    }
+    if (!grpA && eb >= 0) {
+      const int grp = T.ig_group[eb];
+      const int rank = T.grank[grp], rt = (rank + 7) / 8;
+      const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
+      const double* U = Mg + (size_t)rt * kin * 64;
+      const int kt2 = (rank + 3) / 4;
+      const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
+      gt_stage_ct<GT_P, 2, STAGE>(GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt, nullptr, 0, Y,
+                                  sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+    }
+    __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
+    // advance: stage 2 takes chunk i, stage 1 takes chunk i + 1
+    eb = ea < e_end ? ea : -1, cb = ca;
+    if (ea < e_end) advance(ea, ca);
+    if (ea < e_end) {
+      int64_t e2 = ea, c2 = ca;
+      advance(e2, c2);
+      if (grpA) issue_x((i + 1) % 3);             // indices of chunk i+1 were loaded a chunk ago
+      if (e2 < e_end) load_idx((i + 2) % 3, e2, c2);  // buffer of chunk i-1 (done)
+    }
+    ++i;
+  }
+}
+
+static size_t gt_smem_ws(const GTrans& T, bool stage) {
+  const int kin = (T.s_in + 3) / 4;
+  return (size_t)(32 * gt_ld(kin * 4) + 2 * 32 * gt_ld(T.rmax8)) * sizeof(double2) +
+         (stage ? (size_t)T.mmax * sizeof(double) : 0);
+}
+
 static size_t gt_smem(const GTrans& T, int p, int nbuf, bool stage) {
   const int kin = (T.s_in + 3) / 4;
   return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2) +
@@ -610,8 +723,22 @@ static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, 
   k_gtrans<P, NB, STG><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
 }
 
+template <bool STG>
+static void gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans_ws<32, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_gtrans_ws<32, STG><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+}
+
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return;
+  // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
+  static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
+  if (ws_ok && T.atomic && T.all_lowrank) {
+    static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
+                                                           : (size_t)GT_SMEM_BUDGET;
+    if (gt_smem_ws(T, true) <= budget) return gt_launch_ws<true>(T, X, Y, gt_smem_ws(T, true), st);
+    if (gt_smem_ws(T, false) <= budget) return gt_launch_ws<false>(T, X, Y, gt_smem_ws(T, false), st);
+  }
   int p, nb;
   bool stg;
   gt_cfg(T, &p, &nb, &stg);

@@ -55,6 +55,7 @@ struct GTrans {
   const double* pool = nullptr;         // fragment-order matrices
   int s_out = 0, s_in = 0, rmax8 = 0;   // rmax8: largest low rank rounded up to 8
   int64_t mmax = 0;                     // largest matrix block of a group (doubles): shared-memory staging
+  int all_lowrank = 0;                  // every group low rank (warp-specialised kernel)
   int ct1 = 0, ct2 = 0;                 // warp-unit column tiles (experiments: FDA_GT_CT1 / FDA_GT_CT2; 0 = default, -1 = balance)
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
 };

@@ -23,7 +23,8 @@ struct DevLevel {
   int64_t n_out = 0, n_in = 0;
   double2* X = nullptr;
   double2* Y = nullptr;
-  fda::GTrans m2l;  // H6
+  fda::GTrans m2l;   // H6 (groups of rank <= the warp-specialised kernel's limit, or all)
+  fda::GTrans m2l2;  // H6, remaining groups (higher rank / dense), when the level is split
 };
 struct DevTrans {
   int lp = 0, sp = 0, sc = 0;
@@ -421,7 +422,23 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s);
     }
     if (G.out.empty()) continue;
-    P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+    // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
+    // the nearest offsets) go to a second launch of the general kernel.
+    const int rlim = fda::gtrans_ws_rmax(L.s);
+    GroupedPairs G1, G2;
+    for (size_t g = 0; g < G.rank.size(); ++g) {
+      GroupedPairs& D = (G.rank[g] >= 0 && G.rank[g] <= rlim) ? G1 : G2;
+      for (int64_t q = G.gptr[g]; q < G.gptr[g + 1]; ++q) D.out.push_back(G.out[q]), D.in.push_back(G.in[q]);
+      D.gptr.push_back((int64_t)D.out.size());
+      D.rank.push_back(G.rank[g]);
+      D.mat.push_back(G.mat[g]);
+    }
+    if (!G1.out.empty() && !G2.out.empty()) {
+      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+    } else {
+      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+    }
   }
   // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
   // L2L items own child in slots (groups = the same matrices, transposed layout)
@@ -798,6 +815,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
         if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
       for (size_t l = 0; l < P->lv.size(); ++l) {
         fda::launch_gtrans(P->lv[l].m2l, P->lv[l].X, P->lv[l].Y, st);
+        fda::launch_gtrans(P->lv[l].m2l2, P->lv[l].X, P->lv[l].Y, st);
         if (P->lv[l].m2l.n_items) tr("m2l", (int)l);
       }
     }
@@ -828,7 +846,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       if (far) {
         for (const auto& O : P->lo) L += 2 * (O.nleaves > 0) + 2 * (O.nleaves_own > 0);
         for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
-        for (const auto& D : P->lv) L += D.m2l.n_items > 0;
+        for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0);
       }
       P->last_launches = L;
     }

@@ -723,6 +723,15 @@ static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, 
   k_gtrans<P, NB, STG><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
 }
 
+// largest pad8 rank for which the warp-specialised kernel (32 columns, X + 2 T tiles) fits the budget
+int gtrans_ws_rmax(int s_in) {
+  const int kin = (s_in + 3) / 4;
+  int best = 0;
+  for (int r8 = 8; r8 <= 512; r8 += 8)
+    if ((size_t)(32 * gt_ld(kin * 4) + 2 * 32 * gt_ld(r8)) * sizeof(double2) <= (size_t)GT_SMEM_BUDGET) best = r8;
+  return best;
+}
+
 template <bool STG>
 static void gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans_ws<32, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -62,5 +62,6 @@ struct GTrans {
 void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
 int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)
+int gtrans_ws_rmax(int s_in);         // largest (pad8) low rank the warp-specialised kernel takes
 
 }  // namespace fda

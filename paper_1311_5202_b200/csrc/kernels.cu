@@ -320,14 +320,22 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
-                                         int s_out, int nb, int lda_kt = 0, int wbase = 0, int nw = GT_W) {
+                                         int s_out, int nb, int lda_kt = 0, int wbase = 0, int nw = GT_W,
+                                         int* ctr = nullptr, int cbase = 0) {
   if (lda_kt == 0) lda_kt = Kt;  // k tiles per row tile in the fragment-order storage of A
   // the units are spread over warps [wbase, wbase + nw) of the CTA
   const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbase;
   const int CG = GT_P / 8 / GT_CT;
   const int nunits = Mt * CG * ksplit;
   const int g = lane >> 2, t = lane & 3;
-  for (int u = warp; u < nunits; u += nw) {
+  // units: static (warp, warp + nw, ...) or, with ctr, claimed dynamically from a shared counter
+  // (each claimer overshoots once: the counter advances by nunits + #claimers per stage)
+  auto claim = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, v, 0) - cbase;
+  };
+  for (int u = ctr ? claim() : warp; u < nunits; u = ctr ? claim() : u + nw) {
     const int ks = u % ksplit, rest = u / ksplit;
     const int mt = rest / CG, cg = rest - mt * CG;
     const int kb = (ks * Kt) / ksplit, ke = ((ks + 1) * Kt) / ksplit;
@@ -408,14 +416,17 @@ template <int GT_P, int MODE, bool ASM>
 __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ Ag, int Mt, int Kt, int ksplit,
                                             const double2* Bs, int ldb, double2* Ts, int ldt,
                                             double2* __restrict__ Y, const int* sOut, int s_out, int nb,
-                                            int lda_kt = 0, int wbase = 0, int nw = GT_W) {
+                                            int lda_kt = 0, int wbase = 0, int nw = GT_W, int* ctr = nullptr,
+                                            int cbase = 0) {
   if (ct >= 4 && GT_P / 8 >= 4)
     gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt,
-                                                      wbase, nw);
+                                                      wbase, nw, ctr, cbase);
   else if (ct >= 2)
-    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
+    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw, ctr,
+                                 cbase);
   else
-    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
+    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw, ctr,
+                                 cbase);
 }
 
 // One CTA per work item.  Per chunk of GT_P pairs two barriers: [C] after the chunk's gather has
@@ -578,8 +589,10 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   double2* const T0 = gsm2 + GT_P * ldx;  // T double buffer: T0 (even chunks), T0 + GT_P ldt (odd)
   double* Ms = reinterpret_cast<double*>(gsm2 + GT_P * ldx + 2 * GT_P * ldt);
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];
+  __shared__ int bctr;  // stage-2 unit claim counter (monotone; bbase = its value at the stage start)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool grpA = warp < GT_W / 2;  // stage-1 warps (and the gather); the rest run stage 2
+  const bool grpA = warp < GT_W / 2;
+  if (tid == 0) bctr = 0;  // stage-1 warps (and the gather); the rest run stage 2
   const int64_t item = T.item_order[blockIdx.x];
   const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
   if (e_beg >= e_end) return;
@@ -627,7 +640,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   __syncthreads();
   if (grpA) issue_x(0);
   int64_t eb = -1, cb = 0;  // chunk of the stage-2 warps (i - 1); -1: none yet
-  int i = 0;
+  int i = 0, bbase = 0;
   while (ea < e_end || eb >= 0) {
     const int ia = i % 3, ibb = (i + 2) % 3;  // index buffers of chunks i and i - 1
     if (grpA && ea < e_end) {
@@ -640,7 +653,9 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
                                   0, 0, 0, GT_W / 2);
     }
-    if (!grpA && eb >= 0) {
+    if (eb >= 0) {
+      // stage 2 of chunk i-1: its row tiles are claimed dynamically by the stage-2 warps and, once
+      // they are done with stage 1, by the stage-1 warps too (no warp idles at the chunk barrier)
       const int grp = T.ig_group[eb];
       const int rank = T.grank[grp], rt = (rank + 7) / 8;
       const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
@@ -648,7 +663,8 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const int kt2 = (rank + 3) / 4;
       const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
       gt_stage_ct<GT_P, 2, STAGE>(GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt, nullptr, 0, Y,
-                                  sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+                                  sOut[ibb], s_out, nb, 2 * rt, 0, GT_W, &bctr, bbase);
+      bbase += mout + GT_W;  // every warp overshoots the claim counter once
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
     // advance: stage 2 takes chunk i, stage 1 takes chunk i + 1

@@ -589,7 +589,6 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   double2* const T0 = gsm2 + GT_P * ldx;  // T double buffer: T0 (even chunks), T0 + GT_P ldt (odd)
   double* Ms = reinterpret_cast<double*>(gsm2 + GT_P * ldx + 2 * GT_P * ldt);
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];
-  __shared__ int bctr;  // stage-2 unit claim counter (monotone; bbase = its value at the stage start)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool grpA = warp < GT_W / 2;
   if (tid == 0) bctr = 0;  // stage-1 warps (and the gather); the rest run stage 2
@@ -640,7 +639,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   __syncthreads();
   if (grpA) issue_x(0);
   int64_t eb = -1, cb = 0;  // chunk of the stage-2 warps (i - 1); -1: none yet
-  int i = 0, bbase = 0;
+  int i = 0;
   while (ea < e_end || eb >= 0) {
     const int ia = i % 3, ibb = (i + 2) % 3;  // index buffers of chunks i and i - 1
     if (grpA && ea < e_end) {
@@ -653,9 +652,9 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
                                   0, 0, 0, GT_W / 2);
     }
-    if (eb >= 0) {
-      // stage 2 of chunk i-1: its row tiles are claimed dynamically by the stage-2 warps and, once
-      // they are done with stage 1, by the stage-1 warps too (no warp idles at the chunk barrier)
+    if (!grpA && eb >= 0) {
+      // stage 2 of chunk i-1 on warps 4-7 (static units: letting the stage-1 warps claim stage-2 units
+      // from a shared counter measured slower -- 312 vs 300 ms at config 5, more L2 traffic)
       const int grp = T.ig_group[eb];
       const int rank = T.grank[grp], rt = (rank + 7) / 8;
       const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
@@ -663,8 +662,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const int kt2 = (rank + 3) / 4;
       const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
       gt_stage_ct<GT_P, 2, STAGE>(GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt, nullptr, 0, Y,
-                                  sOut[ibb], s_out, nb, 2 * rt, 0, GT_W, &bctr, bbase);
-      bbase += mout + GT_W;  // every warp overshoots the claim counter once
+                                  sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
     // advance: stage 2 takes chunk i, stage 1 takes chunk i + 1

@@ -590,8 +590,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   double* Ms = reinterpret_cast<double*>(gsm2 + GT_P * ldx + 2 * GT_P * ldt);
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool grpA = warp < GT_W / 2;
-  if (tid == 0) bctr = 0;  // stage-1 warps (and the gather); the rest run stage 2
+  const bool grpA = warp < GT_W / 2;  // stage-1 warps (and the gather); the rest run stage 2
   const int64_t item = T.item_order[blockIdx.x];
   const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
   if (e_beg >= e_end) return;

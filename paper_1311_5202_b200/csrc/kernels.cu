@@ -320,22 +320,14 @@ __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
 __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, int Kt, int ksplit, const double2* Bs,
                                          int ldb, double2* Ts, int ldt, double2* __restrict__ Y, const int* sOut,
-                                         int s_out, int nb, int lda_kt = 0, int wbase = 0, int nw = GT_W,
-                                         int* ctr = nullptr, int cbase = 0) {
+                                         int s_out, int nb, int lda_kt = 0, int wbase = 0, int nw = GT_W) {
   if (lda_kt == 0) lda_kt = Kt;  // k tiles per row tile in the fragment-order storage of A
   // the units are spread over warps [wbase, wbase + nw) of the CTA
   const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbase;
   const int CG = GT_P / 8 / GT_CT;
   const int nunits = Mt * CG * ksplit;
   const int g = lane >> 2, t = lane & 3;
-  // units: static (warp, warp + nw, ...) or, with ctr, claimed dynamically from a shared counter
-  // (each claimer overshoots once: the counter advances by nunits + #claimers per stage)
-  auto claim = [&]() {
-    int v = 0;
-    if (lane == 0) v = atomicAdd(ctr, 1);
-    return __shfl_sync(0xffffffffu, v, 0) - cbase;
-  };
-  for (int u = ctr ? claim() : warp; u < nunits; u = ctr ? claim() : u + nw) {
+  for (int u = warp; u < nunits; u += nw) {
     const int ks = u % ksplit, rest = u / ksplit;
     const int mt = rest / CG, cg = rest - mt * CG;
     const int kb = (ks * Kt) / ksplit, ke = ((ks + 1) * Kt) / ksplit;
@@ -416,17 +408,14 @@ template <int GT_P, int MODE, bool ASM>
 __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ Ag, int Mt, int Kt, int ksplit,
                                             const double2* Bs, int ldb, double2* Ts, int ldt,
                                             double2* __restrict__ Y, const int* sOut, int s_out, int nb,
-                                            int lda_kt = 0, int wbase = 0, int nw = GT_W, int* ctr = nullptr,
-                                            int cbase = 0) {
+                                            int lda_kt = 0, int wbase = 0, int nw = GT_W) {
   if (ct >= 4 && GT_P / 8 >= 4)
     gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt,
-                                                      wbase, nw, ctr, cbase);
+                                                      wbase, nw);
   else if (ct >= 2)
-    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw, ctr,
-                                 cbase);
+    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
   else
-    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw, ctr,
-                                 cbase);
+    gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
 }
 
 // One CTA per work item.  Per chunk of GT_P pairs two barriers: [C] after the chunk's gather has

@@ -649,8 +649,8 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const double* U = Mg + (size_t)rt * kin * 64;
       const int kt2 = (rank + 3) / 4;
       const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
-      gt_stage_ct<GT_P, 2, STAGE>(GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt, nullptr, 0, Y,
-                                  sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+      gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
+                                  nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
     // advance: stage 2 takes chunk i, stage 1 takes chunk i + 1

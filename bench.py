@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="5")
     ap.add_argument("--impl", default="fda", choices=["fda", "reference"])
+    ap.add_argument("--kernel", default="bmh", choices=["bmh", "bmg"],
+                    help="operator: Burton-Miller H (the metric's) or G (SURVEY §8(f) row 1)")
     ap.add_argument("--check-rows", type=int, default=2000)
     ap.add_argument("--ref-rows", type=int, default=200)
     ap.add_argument("--no-check", action="store_true")
@@ -163,7 +165,8 @@ def main():
     t_gen = time.time() - t0
     dev = torch.device("cuda", local)
     t0 = time.time()
-    opt = fda.fda_options_default(rank=rank, nranks=world, verbose=1 if args.verbose else 0)
+    kernel = fda.FDA_KERNEL_BMG if args.kernel == "bmg" else fda.FDA_KERNEL_BMH
+    opt = fda.fda_options_default(rank=rank, nranks=world, verbose=1 if args.verbose else 0, kernel=kernel)
     h = fda.fda_plan_create(torch.from_numpy(p.x).to(dev), torch.from_numpy(p.n).to(dev),
                             torch.from_numpy(p.w).to(dev), p.k, p.alpha, p.eps, opt)
     fda.fda_plan_set_correction(h, csr[0], csr[1], csr[2].view(np.float64))
@@ -241,7 +244,8 @@ def main():
         near = d_out.cpu().numpy().view(np.complex128).copy()
         rows = synth.sample_rows(N, args.check_rows, 7)
         t0 = time.perf_counter()
-        ref = oracle.apply_rows(p.x, p.n, p.w, p.k, p.alpha, phi, rows=rows, csr=csr)
+        ref = oracle.apply_rows(p.x, p.n, p.w, p.k, p.alpha, phi, rows=rows, csr=csr,
+                                kind=oracle.KIND_BMG if args.kernel == "bmg" else oracle.KIND_BMH)
         t_or = time.perf_counter() - t0
         if world == 1:
             rel = float(np.linalg.norm(got[rows] - ref) / np.linalg.norm(ref))
@@ -287,7 +291,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "apply_s": ms * 1e-3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": WORKLOADS.get(args.config, args.config), "N": N, "k": p.k, "kD": 2 * p.k,
+                "config": {"workload": WORKLOADS.get(args.config, args.config), "operator": args.kernel.upper(),
+                           "N": N, "k": p.k, "kD": 2 * p.k,
                            "eps": p.eps, "alpha": "i/k", "csr_nnz": int(st["csr_nnz"]),
                            "l2": "inputs larger than L2 (correction CSR %.1f GB)" % (st["csr_nnz"] * 20 / 1e9)},
                 "e2e": {"value": N / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(N * 16),

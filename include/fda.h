@@ -7,6 +7,7 @@
  *   out_i = sum_{j != i} w_j K(x_i, n_i; x_j, n_j) phi_j + sum_{p in row i} val_p phi_{col_p}
  *
  *   K = dG/dn_y + alpha d2G/(dn_x dn_y),  G = e^{ikr}/(4 pi r)      PAPER.md:352-355 (eq_hmat), 210-212
+ *   (or, with fda_options.kernel = FDA_KERNEL_BMG, K = G + alpha dG/dn_x, PAPER.md:356-358 eq_gmat)
  *   far quadrature w_j K(x_i, y_j)                                  PAPER.md:291-297 (eq:far field)
  *   locally corrected kernel K-bar inside D_i, supplied by the caller
  *   as a delta CSR (the "val" term)                                 PAPER.md:329-341 (eq:sum, kcorrection)
@@ -66,6 +67,10 @@ typedef enum {
 #define FDA_PHASE_FAR 4u  /* S2M, M2M, M2L, L2L, L2T (H4-H8)                        */
 #define FDA_PHASE_ALL 7u
 
+/* operator of the plan (fda_options.kernel) */
+#define FDA_KERNEL_BMH 0 /* Burton-Miller H: dipole sources, target (1 + alpha d/dn_x)    */
+#define FDA_KERNEL_BMG 1 /* Burton-Miller G: monopole sources, target (1 + alpha d/dn_x)  */
+
 /* Plan knobs (all optional; fda_options_default fills the defaults). */
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
@@ -80,6 +85,8 @@ typedef struct {
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1) */
   int32_t verbose;         /* plan log (fda_plan_log) */
   double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
+  int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
+                              FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat) */
   int32_t host_only;       /* diagnostics: build the host plan only (tree, lists, operators), no device;
                               fda_apply* then returns FDA_ERR_STATE.  Lets CPU tests audit the lists. */
 } fda_options;

@@ -45,7 +45,7 @@ def _lib():
         L = ctypes.c_int64
         lib.oracle_kernel.argtypes = [ctypes.c_int, V, V, V, V, D, D, D, V]
         lib.oracle_rows.argtypes = [ctypes.c_int, L, V, V, V, D, D, D, V, L, V, V, V, V, V]
-        lib.oracle_near.argtypes = [L, V, V, V, D, D, D, V, L, V, V, V, V, V]
+        lib.oracle_near.argtypes = [ctypes.c_int, L, V, V, V, D, D, D, V, L, V, V, V, V, V]
         lib.oracle_targets.argtypes = [ctypes.c_int, L, V, V, L, V, V, V, D, D, D, V, V]
         lib.oracle_num_threads.restype = ctypes.c_int
         _LIB = lib
@@ -98,14 +98,14 @@ def apply_rows(x, n, w, k, alpha, phi, rows=None, csr=None, kind=KIND_BMH) -> np
     return out
 
 
-def apply_near(x, n, w, k, alpha, phi, leaf_ptr, leaf_pts, pair_ptr, pair_src) -> np.ndarray:
+def apply_near(x, n, w, k, alpha, phi, leaf_ptr, leaf_pts, pair_ptr, pair_src, kind=KIND_BMH) -> np.ndarray:
     """Sum restricted to the listed leaf pairs (j != i).  Leaves are point-index lists."""
     x, n, w = _f64(x), _f64(n), _f64(w)
     phi = _c128(phi)
     N = x.shape[0]
     out = np.zeros(N, dtype=np.complex128)
     a = [np.ascontiguousarray(v, dtype=np.int64) for v in (leaf_ptr, leaf_pts, pair_ptr, pair_src)]
-    _lib().oracle_near(N, _p(x), _p(n), _p(w), float(k), float(np.real(alpha)), float(np.imag(alpha)),
+    _lib().oracle_near(kind, N, _p(x), _p(n), _p(w), float(k), float(np.real(alpha)), float(np.imag(alpha)),
                        _p(phi), a[0].shape[0] - 1, _p(a[0]), _p(a[1]), _p(a[2]), _p(a[3]), _p(out))
     return out
 

@@ -111,13 +111,13 @@ void oracle_rows(int kind, int64_t n, const double *pts, const double *nrm, cons
 }
 
 /*
- * Near-field-only reference: the same sum restricted to the pairs (i, j) with
+ * Near-field-only reference (kernel kind as in oracle_rows): the same sum restricted to the pairs (i, j) with
  * i in target leaf t, j in source leaf s, for the leaf pairs (t, s) listed,
  * j != i.  Leaves are given as point-index lists: leaf_ptr (nleaf+1), leaf_pts.
  * Pairs are grouped by target leaf: pair_ptr (nleaf+1), pair_src.
  * out (2n) is overwritten for every point (zero where no pair contributes).
  */
-void oracle_near(int64_t n, const double *pts, const double *nrm, const double *w,
+void oracle_near(int kind, int64_t n, const double *pts, const double *nrm, const double *w,
                  double k, double ar, double ai, const double *phi,
                  int64_t nleaf, const int64_t *leaf_ptr, const int64_t *leaf_pts,
                  const int64_t *pair_ptr, const int64_t *pair_src, double *out) {
@@ -133,7 +133,7 @@ void oracle_near(int64_t n, const double *pts, const double *nrm, const double *
                 for (int64_t b = leaf_ptr[s]; b < leaf_ptr[s + 1]; ++b) {
                     int64_t j = leaf_pts[b];
                     if (j == i) continue;
-                    cplx kij = kernel(4, pts + 3 * i, nrm + 3 * i, pts + 3 * j, nrm + 3 * j, k, alpha);
+                    cplx kij = kernel(kind, pts + 3 * i, nrm + 3 * i, pts + 3 * j, nrm + 3 * j, k, alpha);
                     acc += w[j] * kij * (phi[2 * j] + I * phi[2 * j + 1]);
                 }
             }

@@ -62,6 +62,7 @@ struct fda_plan_s {
   double2 *q, *phim, *outm, *phi_buf, *out_buf;
   // ownership (multi-GPU)
   int nranks = 1;
+  int kind = 0;  // FDA_KERNEL_BMH / FDA_KERNEL_BMG
   int64_t leaf_b = 0, leaf_e = 0, pt_b = 0, pt_e = 0;
   // correction
   int64_t nnz = 0;
@@ -638,6 +639,8 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     P->host_only = o.host_only != 0;
     P->logstr = P->H.log;
     set_ownership(P.get(), o);
+    if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG) return FDA_ERR_INVALID_ARG;
+    P->kind = o.kernel;
     if (P->host_only) {
       *out = P.release();
       return FDA_OK;
@@ -773,7 +776,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
     const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
     if (!(mask & FDA_PHASE_NEAR) || partial) ck(cudaMemsetAsync(P->outm, 0, (size_t)n * sizeof(double2), st));
     if (mask & FDA_PHASE_NEAR)
-      fda::launch_p2p(P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, Pt, P->q, k, alpha, P->outm,
+      fda::launch_p2p(P->kind, P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, Pt, P->q, k, alpha, P->outm,
                       P->leaf_b, st);
     mark(2);
     if ((mask & FDA_PHASE_CORR) && P->nnz > 0)
@@ -796,7 +799,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       for (auto& D : P->lv)
         if (D.n_out) ck(cudaMemsetAsync(D.X, 0, (size_t)D.n_out * D.s * sizeof(double2), st));
       for (const auto& O : P->lo) {
-        fda::launch_s2m_check(O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, P->surfbuf, st);
+        fda::launch_s2m_check(P->kind, O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, P->surfbuf, st);
         fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st);
         tr("s2m", O.level);
       }

@@ -63,6 +63,17 @@ __device__ __forceinline__ double2 dg_dny(double dx, double dy, double dz, doubl
   return make_double2((-cs - kr * sn) * b, (kr * cs - sn) * b);
 }
 
+// G at d = a - y: e^{ikr}/(4 pi r)   (S2M E_up of the single layer, BM_G plans)
+__device__ __forceinline__ double2 g_only(double dx, double dy, double dz, double k) {
+  const double r2 = dx * dx + dy * dy + dz * dz;
+  const double ir = rsqrt(r2);
+  const double kr = k * r2 * ir;
+  double sn, cs;
+  sincos(kr, &sn, &cs);
+  const double f = FDA_INV4PI * ir;
+  return make_double2(cs * f, sn * f);
+}
+
 // G + alpha dG/dn_x at d = x - y:  e^{ikr}/(4 pi r) [1 + alpha (ikr - 1)(d.n_x)/r^2]   (eq_eval2t)
 __device__ __forceinline__ double2 bm_g(double dx, double dy, double dz, double nxx, double nxy, double nxz,
                                         double k, double2 alpha) {
@@ -116,6 +127,7 @@ void launch_unpermute(int64_t n, const int32_t* perm, const double2* outm, doubl
 // ---------------------------------------------------------------- H2 P2P near field
 #define P2P_T 128
 #define P2P_MAXL 256
+template <int KIND>
 __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_ptr, const int64_t* __restrict__ p2p_ptr,
                                                const int32_t* __restrict__ p2p_src, Points P,
                                                const double2* __restrict__ q, double k, double2 alpha,
@@ -173,7 +185,9 @@ __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_
         if (act) {
           for (int u = my_sl; u < cnt; u += nsl) {
             if (sj[u] == i) continue;
-            const double2 kv = bm_h(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha);
+            const double2 kv =
+                KIND == 0 ? bm_h(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha)
+                          : bm_g(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, k, alpha);
             cfma(acc, kv, sq[u]);
           }
         }
@@ -190,10 +204,13 @@ __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_
     __syncthreads();
   }
 }
-void launch_p2p(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src, Points P,
-                const double2* q, double k, double2 alpha, double2* outm, int64_t leaf0, cudaStream_t st) {
+void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
+                Points P, const double2* q, double k, double2 alpha, double2* outm, int64_t leaf0, cudaStream_t st) {
   if (nleaf <= 0) return;
-  k_p2p<<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
+  if (kind == 0)
+    k_p2p<0><<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
+  else
+    k_p2p<1><<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
 }
 
 // ---------------------------------------------------------------- H3 correction SpMV (warp per row)
@@ -227,6 +244,7 @@ void launch_csr(int64_t r0, int64_t r1, const int64_t* rp, const int32_t* col, c
 // dense group of the grouped-translation kernel (all leaves of a level share S).
 #define S2M_T 128
 #define S2M_MAXC 3
+template <int KIND>
 __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__ leaf_ids, LeafGeom L, Points P,
                                                      const double2* __restrict__ q, const double* __restrict__ surf,
                                                      int nsurf, double k, double2* __restrict__ chk) {
@@ -261,7 +279,10 @@ __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__
         const int i = i0 + threadIdx.x + c * S2M_T;
         if (i >= nsurf) break;
         for (int u = 0; u < cnt; ++u)
-          cfma(acc[c], dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k), sq[u]);
+          cfma(acc[c],
+               KIND == 0 ? dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k)
+                         : g_only(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], k),
+               sq[u]);
       }
     }
 #pragma unroll
@@ -271,10 +292,13 @@ __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__
     }
   }
 }
-void launch_s2m_check(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
+void launch_s2m_check(int kind, int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
                       const double* surf, int nsurf, double k, double2* chk, cudaStream_t st) {
   if (nleaves <= 0) return;
-  k_s2m_check<<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
+  if (kind == 0)
+    k_s2m_check<0><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
+  else
+    k_s2m_check<1><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
 }
 
 // ---------------------------------------------------------------- grouped translation (H5/H6/H7)

@@ -23,6 +23,7 @@ FDA_OK = 0
 STATUS = {0: "FDA_OK", 1: "FDA_ERR_INVALID_ARG", 2: "FDA_ERR_COINCIDENT_POINTS", 3: "FDA_ERR_ALIAS",
           4: "FDA_ERR_CUDA", 5: "FDA_ERR_OOM", 6: "FDA_ERR_SETUP_ACCURACY", 7: "FDA_ERR_NCCL", 8: "FDA_ERR_STATE"}
 FDA_PHASE_NEAR, FDA_PHASE_CORR, FDA_PHASE_FAR, FDA_PHASE_ALL = 1, 2, 4, 7
+FDA_KERNEL_BMH, FDA_KERNEL_BMG = 0, 1
 PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute")
 
 # every symbol include/fda.h declares (checked by tests/test_abi.py)
@@ -37,7 +38,7 @@ class fda_options(ctypes.Structure):
                 ("lf_p_high", ctypes.c_int32), ("lf_p_switch", ctypes.c_double), ("lowrank", ctypes.c_int32),
                 ("single_leaf", ctypes.c_int32), ("hf_max_rows", ctypes.c_int32), ("hf_spacing", ctypes.c_double),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("verbose", ctypes.c_int32),
-                ("eps_lowrank", ctypes.c_double), ("host_only", ctypes.c_int32)]
+                ("eps_lowrank", ctypes.c_double), ("kernel", ctypes.c_int32), ("host_only", ctypes.c_int32)]
 
 
 class fda_stats(ctypes.Structure):

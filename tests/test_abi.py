@@ -46,3 +46,15 @@ def test_options_layout():
     from paper_1311_5202_b200 import fda
     o = fda.fda_options_default()
     assert o.lowrank == 1 and o.nranks == 1 and o.lf_p_low == 6 and o.hf_max_rows > 0
+    assert o.kernel == fda.FDA_KERNEL_BMH and o.eps_lowrank == 0 and o.host_only == 0
+    # the struct layout the binding declares matches the C one: a non-default field round-trips
+    import numpy as np
+    x = np.random.default_rng(0).normal(size=(64, 3))
+    n = x / np.linalg.norm(x, axis=1, keepdims=True)
+    with pytest.raises(fda.FDAError, match="INVALID_ARG"):
+        fda.fda_plan_create(x, n, np.ones(64), 1.0, 1j, 1e-4, fda.fda_options_default(host_only=1, kernel=7))
+    h = fda.fda_plan_create(x, n, np.ones(64), 1.0, 1j, 1e-4,
+                            fda.fda_options_default(host_only=1, kernel=fda.FDA_KERNEL_BMG, rank=1, nranks=2))
+    st = fda.fda_plan_stats(h)
+    fda.fda_plan_destroy(h)
+    assert st["n"] == 64 and 0 < st["owned_begin"] < 64 and st["owned_end"] == 64

@@ -70,6 +70,8 @@ typedef enum {
 /* operator of the plan (fda_options.kernel) */
 #define FDA_KERNEL_BMH 0 /* Burton-Miller H: dipole sources, target (1 + alpha d/dn_x)    */
 #define FDA_KERNEL_BMG 1 /* Burton-Miller G: monopole sources, target (1 + alpha d/dn_x)  */
+#define FDA_KERNEL_T1 2  /* Table-1 summation kernel G + alpha dG/dn_y (eq_sum):
+                            monopole + dipole sources, no target derivative                */
 
 /* Plan knobs (all optional; fda_options_default fills the defaults). */
 typedef struct {
@@ -86,7 +88,9 @@ typedef struct {
   int32_t verbose;         /* plan log (fda_plan_log) */
   double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
   int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
-                              FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat) */
+                              FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat);
+                              FDA_KERNEL_T1: K = G + alpha dG/dn_y (eq_sum; Table 1 mode,
+                              SURVEY §8(f) row 2: pass unit weights and no correction for the paper's summation) */
   int32_t host_only;       /* diagnostics: build the host plan only (tree, lists, operators), no device;
                               fda_apply* then returns FDA_ERR_STATE.  Lets CPU tests audit the lists. */
 } fda_options;

@@ -8,7 +8,8 @@ The arithmetic lives in ``oracle.c`` (plain C, FP64, OpenMP over rows); see its
 header for the definition it computes and the PAPER.md passages it follows.
 This module only marshals numpy arrays through ctypes.
 
-Kernel kinds (``KIND_*``): G, dG/dn_y, dG/dn_x, d2G/dn_x dn_y, BM_H, BM_G.
+Kernel kinds (``KIND_*``): G, dG/dn_y, dG/dn_x, d2G/dn_x dn_y, BM_H, BM_G, and the Table-1 summation
+kernel G + alpha dG/dn_y.
 """
 from __future__ import annotations
 
@@ -21,7 +22,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-KIND_G, KIND_DNY, KIND_DNX, KIND_HYP, KIND_BMH, KIND_BMG = range(6)
+KIND_G, KIND_DNY, KIND_DNX, KIND_HYP, KIND_BMH, KIND_BMG, KIND_T1 = range(7)
 
 
 def build():

@@ -43,7 +43,8 @@
 typedef double complex cplx;
 
 /* kind: 0 = G, 1 = dG/dn_y (double layer), 2 = dG/dn_x (adjoint),
- *       3 = d2G/dn_x dn_y (hypersingular), 4 = BM_H = 1 + alpha*3, 5 = BM_G = 0 + alpha*2 */
+ *       3 = d2G/dn_x dn_y (hypersingular), 4 = BM_H = 1 + alpha*3, 5 = BM_G = 0 + alpha*2,
+ *       6 = Table-1 summation kernel G + alpha dG/dn_y (eq_sum) = 0 + alpha*1 */
 static cplx kernel(int kind, const double *x, const double *nx, const double *y, const double *ny,
                    double k, cplx alpha) {
     double d[3] = {x[0] - y[0], x[1] - y[1], x[2] - y[2]};
@@ -67,6 +68,7 @@ static cplx kernel(int kind, const double *x, const double *nx, const double *y,
     case 3: return hyp;
     case 4: return dny + alpha * hyp;
     case 5: return g + alpha * dnx;
+    case 6: return g + alpha * dny;
     }
     return 0;
 }

@@ -639,7 +639,7 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     P->host_only = o.host_only != 0;
     P->logstr = P->H.log;
     set_ownership(P.get(), o);
-    if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG) return FDA_ERR_INVALID_ARG;
+    if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG && o.kernel != FDA_KERNEL_T1) return FDA_ERR_INVALID_ARG;
     P->kind = o.kernel;
     if (P->host_only) {
       *out = P.release();
@@ -799,7 +799,7 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       for (auto& D : P->lv)
         if (D.n_out) ck(cudaMemsetAsync(D.X, 0, (size_t)D.n_out * D.s * sizeof(double2), st));
       for (const auto& O : P->lo) {
-        fda::launch_s2m_check(P->kind, O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, P->surfbuf, st);
+        fda::launch_s2m_check(P->kind, O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, alpha, P->surfbuf, st);
         fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st);
         tr("s2m", O.level);
       }
@@ -835,7 +835,10 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
         if (!O.nleaves_own) continue;
         ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
         fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st);
-        fda::launch_l2t_eval(O.nleaves_own, O.leaf_own, Lg, Pt, O.surf, O.nsurf, k, alpha, P->surfbuf, P->outm, st);
+        // E_dn = G + alpha dG/dn_x (BM_H, BM_G: PAPER.md eq_eval2t); the Table-1 kernel has no target
+        // derivative: E_dn = G
+        const double2 alpha_dn = P->kind == FDA_KERNEL_T1 ? make_double2(0.0, 0.0) : alpha;
+        fda::launch_l2t_eval(O.nleaves_own, O.leaf_own, Lg, Pt, O.surf, O.nsurf, k, alpha_dn, P->surfbuf, P->outm, st);
         tr("l2t", O.level);
       }
     }

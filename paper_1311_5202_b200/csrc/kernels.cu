@@ -185,9 +185,11 @@ __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_
         if (act) {
           for (int u = my_sl; u < cnt; u += nsl) {
             if (sj[u] == i) continue;
+            // KIND 1: G + alpha dG/dn_x; KIND 2: G + alpha dG/dn_y = the same form with n_x -> -n_y
             const double2 kv =
-                KIND == 0 ? bm_h(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha)
-                          : bm_g(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, k, alpha);
+                KIND == 0   ? bm_h(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha)
+                : KIND == 1 ? bm_g(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, k, alpha)
+                            : bm_g(xi - sx[u], yi - sy[u], zi - sz[u], -snx[u], -sny[u], -snz[u], k, alpha);
             cfma(acc, kv, sq[u]);
           }
         }
@@ -209,8 +211,10 @@ void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t*
   if (nleaf <= 0) return;
   if (kind == 0)
     k_p2p<0><<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
-  else
+  else if (kind == 1)
     k_p2p<1><<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
+  else
+    k_p2p<2><<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm, leaf0);
 }
 
 // ---------------------------------------------------------------- H3 correction SpMV (warp per row)
@@ -247,7 +251,7 @@ void launch_csr(int64_t r0, int64_t r1, const int64_t* rp, const int32_t* col, c
 template <int KIND>
 __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__ leaf_ids, LeafGeom L, Points P,
                                                      const double2* __restrict__ q, const double* __restrict__ surf,
-                                                     int nsurf, double k, double2* __restrict__ chk) {
+                                                     int nsurf, double k, double2 alpha, double2* __restrict__ chk) {
   __shared__ double sx[S2M_T], sy[S2M_T], sz[S2M_T], snx[S2M_T], sny[S2M_T], snz[S2M_T];
   __shared__ double2 sq[S2M_T];
   const int64_t leaf = leaf_ids[blockIdx.x];
@@ -280,8 +284,9 @@ __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__
         if (i >= nsurf) break;
         for (int u = 0; u < cnt; ++u)
           cfma(acc[c],
-               KIND == 0 ? dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k)
-                         : g_only(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], k),
+               KIND == 0   ? dg_dny(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], snx[u], sny[u], snz[u], k)
+               : KIND == 1 ? g_only(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], k)
+                           : bm_g(ax[c] - sx[u], ay[c] - sy[u], az[c] - sz[u], -snx[u], -sny[u], -snz[u], k, alpha),
                sq[u]);
       }
     }
@@ -293,12 +298,14 @@ __global__ void __launch_bounds__(S2M_T) k_s2m_check(const int32_t* __restrict__
   }
 }
 void launch_s2m_check(int kind, int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
-                      const double* surf, int nsurf, double k, double2* chk, cudaStream_t st) {
+                      const double* surf, int nsurf, double k, double2 alpha, double2* chk, cudaStream_t st) {
   if (nleaves <= 0) return;
   if (kind == 0)
-    k_s2m_check<0><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
+    k_s2m_check<0><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, alpha, chk);
+  else if (kind == 1)
+    k_s2m_check<1><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, alpha, chk);
   else
-    k_s2m_check<1><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, chk);
+    k_s2m_check<2><<<(unsigned)nleaves, S2M_T, 0, st>>>(leaf_ids, L, P, q, surf, nsurf, k, alpha, chk);
 }
 
 // ---------------------------------------------------------------- grouped translation (H5/H6/H7)

@@ -24,16 +24,17 @@ struct Points {
 void launch_permute_scale(int64_t n, const int32_t* perm, const double* w, const double2* phi, double2* q,
                           double2* phim, cudaStream_t st);
 void launch_unpermute(int64_t n, const int32_t* perm, const double2* outm, double2* out, cudaStream_t st);
-// kind 0: BM_H kernel (dG/dn_y + alpha d2G/dn_x dn_y), 1: BM_G kernel (G + alpha dG/dn_x)
+// kind 0: BM_H kernel (dG/dn_y + alpha d2G/dn_x dn_y), 1: BM_G kernel (G + alpha dG/dn_x),
+// 2: Table-1 kernel (G + alpha dG/dn_y)
 void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
                 Points P, const double2* q, double k, double2 alpha, double2* outm, int64_t tgt_leaf_begin,
                 cudaStream_t st);
 void launch_csr(int64_t row_begin, int64_t row_end, const int64_t* rp, const int32_t* col, const double2* val,
                 const double2* phim, double2* outm, cudaStream_t st);
 // H4: check potentials chk[t][i] of leaf leaf_ids[t] on its check surface (nsurf points, relative):
-// kind 0 dipole sources (dG/dn_y), kind 1 monopole sources (G)
+// kind 0 dipole sources (dG/dn_y), 1 monopole sources (G), 2 monopole + alpha dipole (G + alpha dG/dn_y)
 void launch_s2m_check(int kind, int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double2* q,
-                      const double* surf, int nsurf, double k, double2* chk, cudaStream_t st);
+                      const double* surf, int nsurf, double k, double2 alpha, double2* chk, cudaStream_t st);
 // H8: out += E_dn rho over the leaves' equivalent surfaces; rho[t][b] for leaf leaf_ids[t]
 void launch_l2t_eval(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double* surf, int nsurf,
                      double k, double2 alpha, const double2* rho, double2* outm, cudaStream_t st);

@@ -23,7 +23,7 @@ FDA_OK = 0
 STATUS = {0: "FDA_OK", 1: "FDA_ERR_INVALID_ARG", 2: "FDA_ERR_COINCIDENT_POINTS", 3: "FDA_ERR_ALIAS",
           4: "FDA_ERR_CUDA", 5: "FDA_ERR_OOM", 6: "FDA_ERR_SETUP_ACCURACY", 7: "FDA_ERR_NCCL", 8: "FDA_ERR_STATE"}
 FDA_PHASE_NEAR, FDA_PHASE_CORR, FDA_PHASE_FAR, FDA_PHASE_ALL = 1, 2, 4, 7
-FDA_KERNEL_BMH, FDA_KERNEL_BMG = 0, 1
+FDA_KERNEL_BMH, FDA_KERNEL_BMG, FDA_KERNEL_T1 = 0, 1, 2
 PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute")
 
 # every symbol include/fda.h declares (checked by tests/test_abi.py)

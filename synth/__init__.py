@@ -100,6 +100,42 @@ def octa_sphere(nu: int, radius: float = 1.0) -> np.ndarray:
     return nodes
 
 
+def cube_sphere(m: int, radius: float = 1.0) -> np.ndarray:
+    """Equiangular cube-sphere of curved quadratic triangles: m x m cells per cube face, 2 triangles per
+    cell, 12 m^2 elements, N = 72 m^2 quadrature points -- the point counts of PAPER.md Table 1
+    (73,728 * 4^j at m = 32 * 2^j).  Nodes: corners and mid-edges in the face's angular
+    coordinates mapped radially onto the sphere; counter-clockwise seen from outside."""
+    t = np.linspace(-np.pi / 4, np.pi / 4, 2 * m + 1)          # half-cell steps (mid-edge nodes)
+    elems = []
+    for ax in range(3):
+        for sgn in (1.0, -1.0):
+            o0, o1 = [a for a in range(3) if a != ax]
+
+            def P(i, j):
+                v = np.zeros(np.broadcast(i, j).shape + (3,))
+                v[..., ax] = sgn
+                v[..., o0] = np.tan(t[i])
+                v[..., o1] = np.tan(t[j])
+                return v
+
+            I, J = np.meshgrid(np.arange(m), np.arange(m), indexing="ij")
+            a, b = 2 * I.ravel(), 2 * J.ravel()
+            # two triangles per cell: (00, 20, 22) and (00, 22, 02) in half-step indices
+            for (i1, j1), (i2, j2), (i3, j3) in (((0, 0), (2, 0), (2, 2)), ((0, 0), (2, 2), (0, 2))):
+                c1, c2, c3 = P(a + i1, b + j1), P(a + i2, b + j2), P(a + i3, b + j3)
+                m12 = P(a + (i1 + i2) // 2, b + (j1 + j2) // 2)
+                m23 = P(a + (i2 + i3) // 2, b + (j2 + j3) // 2)
+                m31 = P(a + (i3 + i1) // 2, b + (j3 + j1) // 2)
+                elems.append(np.stack([c1, c2, c3, m12, m23, m31], axis=1))
+    nodes = np.concatenate(elems, axis=0)
+    nodes = radius * nodes / np.linalg.norm(nodes, axis=-1, keepdims=True)
+    e1 = nodes[:, 1] - nodes[:, 0]
+    e2 = nodes[:, 2] - nodes[:, 0]
+    flip = np.einsum('ij,ij->i', np.cross(e1, e2), nodes[:, :3].mean(axis=1)) < 0
+    nodes[flip] = nodes[flip][:, [0, 2, 1, 5, 4, 3]]
+    return nodes
+
+
 def spheroid(a: float, b: float, h: float) -> np.ndarray:
     """Prolate spheroid x^2/a^2 + (y^2+z^2)/b^2 = 1 meshed by rings.
 
@@ -330,6 +366,11 @@ CONFIGS = {
     "3": ("sphere", 91, 50.0),
     "4": ("spheroid", 0.0366, 20.0),
     "5": ("sphere", 289, 500.0),
+    # Table-1 workloads: cube-sphere, ~20 points per wavelength, N = 73,728 * 4^j
+    "t1": ("cubesphere", 32, 8 * np.pi),
+    "t1b": ("cubesphere", 64, 16 * np.pi),
+    "t1c": ("cubesphere", 128, 32 * np.pi),
+    "t1d": ("cubesphere", 256, 64 * np.pi),
 }
 
 
@@ -341,6 +382,8 @@ def make_problem(name: str, eps: float = 1e-4, k: float | None = None, nu: int |
         par = nu
     if geo == "sphere":
         nodes = octa_sphere(int(par), 1.0)
+    elif geo == "cubesphere":
+        nodes = cube_sphere(int(par), 1.0)
     else:
         nodes = spheroid(10.0, 1.0, float(par))
     x, n, w, hmax, samples = quadrature_cloud(nodes)

@@ -279,3 +279,19 @@ def test_oracle_rows_subset_linearity_and_near():
     K = np.array([[0 if i == j else p.w[j] * oracle.kernel(4, p.x[i], p.n[i], p.x[j], p.n[j], p.k, p.alpha)
                    for j in range(n)] for i in range(0, n, 9)])
     assert np.abs(K @ phi1 - full1[::9]).max() < 1e-12 * np.abs(full1).max()
+
+
+def test_p3_table1_kernel_reciprocity():
+    """Kind 6, the Table-1 summation kernel G + alpha dG/dn_y, is the BM_G kernel with
+    the roles of the two points exchanged: K_T1(x, n_x; y, n_y) = K_G(y, n_y; x, n_x) (G symmetric,
+    d/dn_y acting on the second argument); and it is the sum of the separately pinned G and dG/dn_y."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        x, y = rng.normal(size=3), rng.normal(size=3)
+        a, b = _rand_unit(rng), _rand_unit(rng)
+        k = rng.uniform(0.1, 30)
+        al = complex(rng.normal(), rng.normal())
+        t1 = oracle.kernel(oracle.KIND_T1, x, a, y, b, k, al)
+        assert abs(t1 - oracle.kernel(oracle.KIND_BMG, y, b, x, a, k, al)) <= 1e-14 * abs(t1)
+        parts = oracle.kernel(oracle.KIND_G, x, None, y, None, k) + al * oracle.kernel(oracle.KIND_DNY, x, None, y, b, k)
+        assert abs(t1 - parts) <= 1e-14 * abs(t1)

@@ -94,3 +94,20 @@ def test_phi_seeded():
     b = synth.random_phi(100, 5)
     assert np.array_equal(a, b)
     assert np.all(np.abs(a.real) <= 1) and np.all(np.abs(a.imag) <= 1)
+
+
+def test_cube_sphere_table1_counts_and_geometry():
+    """Table-1 point sets: N = 72 m^2 = 73,728 at m = 32; outward unit normals,
+    area -> 4 pi at >= third order under m -> 2m."""
+    import numpy as np
+    import synth
+    nd = synth.cube_sphere(32)
+    assert nd.shape[0] * 6 == 73728
+    errs = []
+    for m in (4, 8, 16):
+        x, n, w, hmax, s = synth.quadrature_cloud(synth.cube_sphere(m))
+        assert x.shape[0] == 72 * m * m
+        assert np.abs(np.linalg.norm(n, axis=1) - 1).max() < 1e-12
+        assert np.all(np.einsum("ij,ij->i", n, x) > 0)
+        errs.append(abs(w.sum() - 4 * np.pi))
+    assert errs[1] / errs[2] > 7.0 and errs[0] / errs[1] > 7.0

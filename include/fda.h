@@ -77,7 +77,8 @@ typedef enum {
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
   double eps_internal;     /* expansion truncation (R+ SVDs, HF interpolative selection); 0 -> eps / 100 (R11) */
-  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6) */
+  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6; for eps < 1e-4 the
+                              plan adds round(log10(1e-4 / eps)) points per edge to both lf_p_low and lf_p_high) */
   int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths (default 8) */
   double lf_p_switch;      /* w / lambda switch (default 0.75) */
   int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */

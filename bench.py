@@ -36,15 +36,18 @@ WORKLOADS = {
 }
 
 
-def fp64_peak_tflops(sm_mhz: float):
-    """FP64 roofline peak: the measured DFMA / DMMA figure (profiles/fp64_peak_r01.json, tools/fp64_peak.cu),
-    else derived from the unit counts 148 SM x 64 FP64 FMA/clk x 2 flop x clock."""
-    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+def fp64_peaks(sm_mhz: float):
+    """FP64 roofline peaks {"alu": DFMA, "tensor": DMMA} in TFLOP/s: measured on this pool's B200 by
+    tools/fp64_peak.py (profiles/fp64_peak_r02.json, with its clock record; MEASURED_PEAKS.json has no FP64
+    figure), else derived from the unit counts 148 SM x 64 FP64 FMA/clk x 2 flop x clock."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r02.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return max(d["dfma_tflops"], d["dmma_tflops"]), "measured FP64 (tools/fp64_peak.cu: max of DFMA, DMMA)"
-    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12, "derived FP64 DFMA peak: 148 SM x 64 FMA/clk x 2 x sm_max_mhz"
+        src = "measured (tools/fp64_peak.py, profiles/fp64_peak_r02.json)"
+        return {"alu": d["dfma_tflops"], "tensor": d["dmma_tflops"]}, src
+    v = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+    return {"alu": v, "tensor": v}, "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"
 
 
 def measured_peaks():
@@ -158,17 +161,26 @@ def main():
     from paper_1311_5202_b200 import fda
 
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
     p, csr, phi = make_inputs(args.config)
     t_gen = time.time() - t0
-    dev = torch.device("cuda", local)
     t0 = time.time()
     kernel = fda.FDA_KERNEL_BMG if args.kernel == "bmg" else fda.FDA_KERNEL_BMH
-    opt = fda.fda_options_default(rank=rank, nranks=world, verbose=1 if args.verbose else 0, kernel=kernel)
-    h = fda.fda_plan_create(torch.from_numpy(p.x).to(dev), torch.from_numpy(p.n).to(dev),
-                            torch.from_numpy(p.w).to(dev), p.k, p.alpha, p.eps, opt)
+    opt = fda.fda_options_default(verbose=1 if args.verbose else 0, kernel=kernel)
+    pts, nrm, wts = (torch.from_numpy(a).to(dev) for a in (p.x, p.n, p.w))
+    if world > 1:
+        # the library's own data plane: NCCL communicator inside libfda, partial-expansion
+        # exchange + output all-gather inside fda_apply; the process group only distributes the NCCL id
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(fda.fda_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        h = fda.fda_plan_create_dist(pts, nrm, wts, p.k, p.alpha, p.eps, bytes(uid.cpu().numpy()), rank, world, opt)
+    else:
+        h = fda.fda_plan_create(pts, nrm, wts, p.k, p.alpha, p.eps, opt)
     fda.fda_plan_set_correction(h, csr[0], csr[1], csr[2].view(np.float64))
     t_plan = time.time() - t0
     stream = torch.cuda.current_stream(dev)
@@ -180,22 +192,14 @@ def main():
     d_out = torch.empty_like(d_phi)
     N = p.N
 
-    def step(timed_phases=None):
-        if timed_phases is not None:
-            ms = fda.fda_apply_timed(h, fda.FDA_PHASE_ALL, d_phi, d_out)
-            for key, v in ms.items():
-                timed_phases[key] = timed_phases.get(key, 0.0) + v
-        else:
-            fda.fda_apply(h, d_phi, d_out)
-        if world > 1:
-            dist.all_reduce(d_out)   # owned rows are disjoint, the rest zero: the sum assembles out
+    def step():
+        fda.fda_apply(h, d_phi, d_out)     # multi-GPU: exchange + output all-gather inside (full out on every rank)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # ---- timed region (device time, CUDA events on the launching stream)
     clocks = Clocks(local)
-    phases = {}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -203,7 +207,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step(phases)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     launches_step = launches_per_step(h)
@@ -216,6 +220,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = N / (ms * 1e-3) / 1e6
+    # ---- per-phase CUDA-event times (separate applies after the timed region; phases serialised)
+    phases = {}
+    for _ in range(args.steps):
+        for key, v in fda.fda_apply_timed(h, fda.FDA_PHASE_ALL, d_phi, d_out).items():
+            phases[key] = phases.get(key, 0.0) + v
+    torch.cuda.synchronize()
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside the timed region
     h_phi = torch.from_numpy(phi.view(np.float64)).pin_memory()
@@ -236,21 +246,21 @@ def main():
     # ---- parity at full size on seeded sampled rows (oracle, outside the timed region; rank 0)
     parity = None
     cpu_baseline = None
-    if rank == 0 and not args.no_check:
-        import oracle
+    if not args.no_check:      # the applies are collective on every rank; the oracle runs on rank 0
         fda.fda_apply(h, d_phi, d_out)
         got = d_out.cpu().numpy().view(np.complex128).copy()
         fda.fda_apply_phases(h, fda.FDA_PHASE_NEAR | fda.FDA_PHASE_CORR, d_phi, d_out)
         near = d_out.cpu().numpy().view(np.complex128).copy()
+    if rank == 0 and not args.no_check:
+        import oracle
         rows = synth.sample_rows(N, args.check_rows, 7)
         t0 = time.perf_counter()
         ref = oracle.apply_rows(p.x, p.n, p.w, p.k, p.alpha, phi, rows=rows, csr=csr,
                                 kind=oracle.KIND_BMG if args.kernel == "bmg" else oracle.KIND_BMH)
         t_or = time.perf_counter() - t0
-        if world == 1:
-            rel = float(np.linalg.norm(got[rows] - ref) / np.linalg.norm(ref))
-            far = float(np.linalg.norm((got[rows] - near[rows]) - (ref - near[rows])) / np.linalg.norm(ref - near[rows]))
-            parity = {"rows": int(rows.shape[0]), "rel_l2": rel, "far_rel_l2": far, "tol": 1e-4, "pass": rel <= 1e-4}
+        rel = float(np.linalg.norm(got[rows] - ref) / np.linalg.norm(ref))
+        far = float(np.linalg.norm((got[rows] - near[rows]) - (ref - near[rows])) / np.linalg.norm(ref - near[rows]))
+        parity = {"rows": int(rows.shape[0]), "rel_l2": rel, "far_rel_l2": far, "tol": 1e-4, "pass": rel <= 1e-4}
         cpu_v = rows.shape[0] / t_or / 1e6
         cpu_baseline = {"value": cpu_v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                         "sample": f"{rows.shape[0]} seeded rows of the full N={N} operator (direct sum + CSR), "
@@ -268,7 +278,7 @@ def main():
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
-    peak64, peak_src = fp64_peak_tflops(pk.get("sm_max_mhz", 1965.0))
+    peak64, peak_src = fp64_peaks(pk.get("sm_max_mhz", 1965.0))
     # bound of each phase: the translations run on the FP64 tensor pipe (DMMA), P2P / surface
     # evaluations on the FP64 ALU (sincos, rsqrt, DFMA), the correction SpMV on HBM
     bound = {"m2l": "tensor", "m2m": "tensor", "l2l": "tensor", "p2p": "alu", "s2m": "alu", "l2t": "alu"}
@@ -279,8 +289,9 @@ def main():
             return {"bound": "hbm", "achieved": a, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": a / pk["hbm_gbs"],
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}
         a = flops.get(ph, 0.0) / (per[ph] * 1e-3) / 1e12
-        return {"bound": bound.get(ph, "alu"), "achieved": a, "peak": peak64, "unit": "TFLOP/s", "frac": a / peak64,
-                "peak_source": peak_src}
+        b = bound.get(ph, "alu")
+        return {"bound": b, "achieved": a, "peak": peak64[b], "unit": "TFLOP/s", "frac": a / peak64[b],
+                "peak_source": f"FP64 {'DMMA' if b == 'tensor' else 'DFMA'} peak, {peak_src}"}
 
     roof = dict(phase_roof(dom), traffic=traffic, kernel=dom)
     roof_phases = {ph: {k_: (round(v, 4) if isinstance(v, float) else v) for k_, v in phase_roof(ph).items()
@@ -292,6 +303,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms, "apply_s": ms * 1e-3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOADS.get(args.config, args.config), "operator": args.kernel.upper(),
+                           "parallelism": "single GPU" if world == 1 else
+                           f"{world} Morton leaf ranges, NCCL partial-expansion exchange + output all-gather",
                            "N": N, "k": p.k, "kD": 2 * p.k,
                            "eps": p.eps, "alpha": "i/k", "csr_nnz": int(st["csr_nnz"]),
                            "l2": "inputs larger than L2 (correction CSR %.1f GB)" % (st["csr_nnz"] * 20 / 1e9)},
@@ -304,7 +317,8 @@ def main():
                             "lists": st["setup_lists_s"], "ops": st["setup_ops_s"], "upload": st["setup_upload_s"]},
                 "plan": {k_: st[k_] for k_ in ("nleaves", "nlevels", "lmin", "p2p_point_pairs", "m2l_pairs",
                                                "m2l_groups", "m2l_lowrank_groups", "out_slots", "in_slots",
-                                               "device_bytes")}}
+                                               "device_bytes", "s2m_evals", "l2t_evals", "xchg_send_bytes",
+                                               "xchg_recv_bytes")}}
         line["gpu_launches"] = launches_step * args.steps
         print(json.dumps(line), flush=True)
     fda.fda_plan_destroy(h)

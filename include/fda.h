@@ -36,6 +36,11 @@
  *   FDA_ERR_ALIAS         phi and out are the same buffer
  *   FDA_ERR_CUDA          a CUDA error (sticky: destroy the plan)
  *   FDA_ERR_OOM           device allocation failed
+ *   FDA_ERR_SETUP_ACCURACY the plan cannot reach eps on this device (a translation launch needs more shared
+ *                         memory than the device has, at very small eps)
+ *   FDA_ERR_NCCL          NCCL missing or a collective failed (multi-GPU plans)
+ *   FDA_ERR_STATE         call not valid for this plan (host_only plan; fda_apply on a partitioned plan
+ *                         without communicator)
  * Threading: one apply in flight per plan; the device-pointer apply is ordered on
  * the plan's stream (fda_plan_set_stream) and does not synchronise the host.
  */
@@ -61,6 +66,9 @@ typedef enum {
   FDA_ERR_STATE = 8
 } fda_status;
 
+/* number of phase times fda_apply_timed writes */
+#define FDA_NPHASES 10
+
 /* phase mask for fda_apply_phases (tests / diagnostics) */
 #define FDA_PHASE_NEAR 1u /* P2P over the plan's near leaf pairs (H2)             */
 #define FDA_PHASE_CORR 2u /* correction CSR (H3)                                   */
@@ -77,15 +85,17 @@ typedef enum {
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
   double eps_internal;     /* expansion truncation (R+ SVDs, HF interpolative selection); 0 -> eps / 100 (R11) */
-  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch (default 6; for eps < 1e-4 the
-                              plan adds round(log10(1e-4 / eps)) points per edge to both lf_p_low and lf_p_high) */
-  int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths (default 8) */
+  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch; 0 (default) -> 6 + dp with
+                              dp = round(log10(1e-4 / eps)) for eps < 1e-4, else 0 (R17); a value > 1 is
+                              used verbatim */
+  int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths; 0 (default) -> 8 + dp */
   double lf_p_switch;      /* w / lambda switch (default 0.75) */
   int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */
   int32_t single_leaf;     /* debug: no far field, every pair P2P (default 0) */
   int32_t hf_max_rows;     /* HF directional-set sample rows (default 6000) */
   double hf_spacing;       /* HF candidate spacing in wavelengths (default 0.25) */
-  int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1) */
+  int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1);
+                              nranks <= 64; see fda_plan_create_dist / fda_apply_up */
   int32_t verbose;         /* plan log (fda_plan_log) */
   double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
   int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
@@ -108,6 +118,8 @@ typedef struct {
   double setup_tree_s, setup_lists_s, setup_ops_s, setup_upload_s;
   double flops_p2p, flops_m2l, flops_m2m, flops_l2l, flops_s2m, flops_l2t; /* algorithmic flops per apply */
   double bytes_csr;                                                        /* algorithmic bytes of H3 per apply */
+  int64_t s2m_evals, l2t_evals;               /* kernel evaluations of the S2M / L2T surface phases per apply */
+  int64_t xchg_send_bytes, xchg_recv_bytes;   /* multi-GPU: expansion bytes this rank sends / receives per apply */
 } fda_stats;
 
 void fda_options_default(fda_options* opt);
@@ -131,8 +143,9 @@ fda_status fda_plan_set_correction(fda_plan plan, int64_t nnz, const int64_t* ro
 fda_status fda_apply(fda_plan plan, const double* phi, double* out);
 /* Same, restricted to the phases in mask (FDA_PHASE_*). */
 fda_status fda_apply_phases(fda_plan plan, uint32_t mask, const double* phi, double* out);
-/* Same as fda_apply_phases, with CUDA-event time per phase written to phase_ms[0..8]:
- * permute, p2p, csr, s2m, m2m, m2l, l2l, l2t, unpermute (device pointers only; synchronises). */
+/* Same as fda_apply_phases, with CUDA-event time per phase written to phase_ms[0..FDA_NPHASES-1]:
+ * permute, p2p, csr, s2m, m2m (+ pack), m2l (+ unpack), l2l, l2t, unpermute (+ output all-gather), exchange
+ * (device pointers only; synchronises; phases run one after another, without the exchange overlap). */
 fda_status fda_apply_timed(fda_plan plan, uint32_t mask, const double* phi, double* out, float* phase_ms);
 
 /* Order the plan's device work on this cudaStream_t (default: the legacy default stream). */
@@ -150,6 +163,41 @@ fda_status fda_plan_export_leaves(fda_plan plan, int64_t* nleaves, int32_t* leaf
 fda_status fda_plan_export_p2p(fda_plan plan, int64_t* npairs, int32_t* tgt_leaf, int32_t* src_leaf);
 /* The M2L cube pairs: level, target cube ijk (3), source cube ijk (3). */
 fda_status fda_plan_export_m2l(fda_plan plan, int64_t* npairs, int32_t* level, int64_t* tgt_ijk, int64_t* src_ijk);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU.  Rank q of R owns a contiguous Morton range of leaves (cut by estimated work) and
+ * computes the rows of out in it: P2P, correction, S2M on its leaves, M2M on the cubes holding its points
+ * (partial expansions: M2M is linear), M2L into target cubes holding its points, L2L, L2T.  Before M2L each
+ * rank receives from the other ranks of every source cube it reads their partial outgoing expansions
+ * (the upward pass of PAPER.md:519-523 split by points, summed on arrival) -- one grouped NCCL
+ * send/receive per apply, overlapped with P2P and the correction -- and after L2T the ranks' rows are
+ * all-gathered, so every rank returns the full out. */
+
+/* 128-byte NCCL unique id (ncclGetUniqueId); rank 0 makes it, the caller distributes it.
+ * FDA_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+fda_status fda_nccl_unique_id(char* id);
+/* Collective over the nranks processes (each on its own current device): builds the same plan on every rank
+ * (opt->rank / opt->nranks are overridden) and the NCCL communicator.  fda_apply on the plan then returns the
+ * full out on every rank.  Errors as fda_plan_create_ex, FDA_ERR_NCCL if the communicator fails. */
+fda_status fda_plan_create_dist(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                                double k, double alpha_re, double alpha_im, double eps, const fda_options* opt,
+                                const char* nccl_id, int rank, int nranks, fda_plan* out);
+
+/* The exchange without NCCL (tests, other transports).  A plan made by fda_plan_create_ex with
+ * opt.nranks > 1 (no communicator) rejects fda_apply (FDA_ERR_STATE) and is applied in two halves:
+ *   fda_dist_counts: complex128 elements this rank sends to / receives from each peer (nranks entries each);
+ *   fda_apply_up:    permute + S2M + M2M, packs the partial expansions into sendbuf (device, peer-major);
+ *   fda_apply_down:  adds recvbuf (device, peer-major; the bytes peer q sent to this rank, in q order), then
+ *                    P2P, correction, M2L, L2L, L2T; out (device, caller order) holds this rank's rows, the
+ *                    other rows zero.
+ * Device pointers only (FDA_ERR_INVALID_ARG otherwise); stream-ordered like fda_apply. */
+fda_status fda_dist_counts(fda_plan plan, int64_t* send_counts, int64_t* recv_counts);
+fda_status fda_apply_up(fda_plan plan, const double* phi, double* sendbuf);
+fda_status fda_apply_down(fda_plan plan, const double* recvbuf, double* out);
+/* Diagnostics (also for host_only plans): the exchange list with peer (recv = 0: what this rank sends to peer,
+ * 1: what it receives from peer) in buffer order: level, out slot and cube ijk (3 per entry). */
+fda_status fda_plan_export_exchange(fda_plan plan, int peer, int recv, int64_t* count, int32_t* level, int64_t* slot,
+                                    int64_t* cube_ijk);
 
 fda_status fda_plan_destroy(fda_plan plan);
 const char* fda_status_str(fda_status s);

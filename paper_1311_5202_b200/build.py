@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfda.so")
-SOURCES = ["api.cu", "kernels.cu", "plan.cpp", "linalg.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "plan.cpp", "linalg.cpp", "nccl_dl.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOSTFLAGS = "-O3,-fPIC,-fopenmp,-march=x86-64-v3,-fcx-limited-range"
 
@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("libfda build failed")
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler",
-                           HOSTFLAGS, *objs, "-o", tmp, "-lgomp", "-lcudart"])
+                           HOSTFLAGS, *objs, "-o", tmp, "-lgomp", "-lcudart", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -12,16 +12,25 @@
 
 #include "../../include/fda.h"
 #include "kernels.cuh"
+#include "nccl_dl.hpp"
 #include "plan.hpp"
 
 using fda::cplx;
+
+// FP64 flops per kernel evaluation (P2P point pair; S2M / L2T surface evaluation) by operator kind
+// (BM_H, BM_G, T1): (2 x DFMA + DADD + DMUL) thread instructions per evaluation of k_p2p / k_s2m_check /
+// k_l2t_eval, counted by ncu (profiles/r02_fp64_counts.md); they turn the evaluation counts into the
+// algorithmic flops the roofline fractions of the ALU phases use.
+static const double FLOP_P2P[3] = {100.0, 60.0, 60.0};
+static const double FLOP_S2M[3] = {40.0, 30.0, 60.0};
+static const double FLOP_L2T = 60.0;
 
 namespace {
 
 struct DevLevel {
   int s = 0;
   int64_t n_out = 0, n_in = 0;
-  double2* X = nullptr;
+  double2* X = nullptr;  // = Xall + xoff of this level (all levels' outgoing expansions are one allocation)
   double2* Y = nullptr;
   fda::GTrans m2l;   // H6 (groups of rank <= the warp-specialised kernel's limit, or all)
   fda::GTrans m2l2;  // H6, remaining groups (higher rank / dense), when the level is split
@@ -33,9 +42,8 @@ struct DevTrans {
 };
 struct DevLeafOps {
   int level = 0, s = 0, nsurf = 0;
-  int64_t nleaves = 0;       // all leaves of the level (S2M)
-  int64_t nleaves_own = 0;   // owned leaves (L2T)
-  int32_t *leaf = nullptr, *leaf_own = nullptr;
+  int64_t nleaves_own = 0;   // owned leaves of the level (S2M and L2T)
+  int32_t* leaf_own = nullptr;
   double* surf = nullptr;
   fda::GTrans s2m;           // H4 reduction: X[slot] += S chk[t]            (S = Sigma^-1 U^H, eq_cmps)
   fda::GTrans l2t;           // H8 reduction: rho[t'] += T Y[slot]           (T = conj(U) Sigma^-1, eq_cmpt)
@@ -60,10 +68,26 @@ struct fda_plan_s {
   int64_t *p2p_ptr;
   int32_t* p2p_src;
   double2 *q, *phim, *outm, *phi_buf, *out_buf;
-  // ownership (multi-GPU)
-  int nranks = 1;
-  int kind = 0;  // FDA_KERNEL_BMH / FDA_KERNEL_BMG
+  // ownership (multi-GPU): rank q owns Morton leaves [rank_leaf[q], rank_leaf[q+1]) = points
+  // [rank_pt[q], rank_pt[q+1])
+  int nranks = 1, rank = 0;
+  int kind = 0;  // FDA_KERNEL_BMH / FDA_KERNEL_BMG / FDA_KERNEL_T1
   int64_t leaf_b = 0, leaf_e = 0, pt_b = 0, pt_e = 0;
+  std::vector<int64_t> rank_pt, rank_leaf;
+  // expansion exchange: send entries (peer-major, (level, slot) ascending) and received partial sums
+  struct Xchg {
+    std::vector<std::vector<std::pair<int, int64_t>>> send, recv;  // per peer: (level, out slot)
+    std::vector<int64_t> send_cnt, recv_cnt;                       // per peer, complex128 elements
+    int64_t send_tot = 0, recv_tot = 0, nsend = 0, ndst = 0;
+    int64_t *s_xoff = nullptr, *s_boff = nullptr, *d_xoff = nullptr, *d_rptr = nullptr, *d_roff = nullptr;
+    int32_t *s_len = nullptr, *d_len = nullptr;
+    double2 *sendbuf = nullptr, *recvbuf = nullptr;
+  } xc;
+  double2* Xall = nullptr;
+  std::vector<int64_t> xoff;  // per level offset (complex128 elements) into Xall
+  ncclComm_t comm = nullptr;  // fda_plan_create_dist
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_x = nullptr;
   // correction
   int64_t nnz = 0;
   int64_t* c_ptr = nullptr;
@@ -331,8 +355,10 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   return T;
 }
 
-// Ownership (multi-GPU): rank r of R owns the contiguous leaf range whose points
-// start at or after floor(n r / R) and before floor(n (r+1) / R) (leaves are never split).
+// Ownership (multi-GPU): the leaves (Morton order) are cut into nranks contiguous ranges of
+// about equal estimated work -- P2P point pairs x 100 flop + the M2L flops into every ancestor cube, shared
+// among the cube's leaves by points + the leaf's S2M / L2T surface work.  Leaves are never
+// split, so a rank owns whole leaves and the point range they span.
 void set_ownership(fda_plan P, const fda_options& o) {
   const fda::HostPlan& H = P->H;
   const int64_t n = H.n, nl = (int64_t)H.leaves.size();
@@ -340,22 +366,127 @@ void set_ownership(fda_plan P, const fda_options& o) {
   for (int64_t t = 0; t < nl; ++t) lp[t] = H.cubes[H.leaves[t]].pbeg;
   lp[nl] = n;
   const int R = std::max(1, o.nranks), r = std::min(std::max(0, o.rank), R - 1);
-  const int64_t pb = (n * r) / R, pe = (n * (r + 1)) / R;
-  int64_t lb = std::lower_bound(lp.begin(), lp.begin() + nl, pb) - lp.begin();
-  int64_t le = std::lower_bound(lp.begin(), lp.begin() + nl, pe) - lp.begin();
-  if (r == R - 1) le = nl;
-  if (r == 0) lb = 0;
+  std::vector<int64_t> rl(R + 1, 0);
+  rl[R] = nl;
+  if (R > 1) {
+    std::vector<double> cost(nl, 0.0);
+    for (int64_t t = 0; t < nl; ++t) {
+      double src = 0;
+      for (int64_t e = H.p2p_ptr[t]; e < H.p2p_ptr[t + 1]; ++e) src += (double)(lp[H.p2p_src[e] + 1] - lp[H.p2p_src[e]]);
+      const double nt = (double)(lp[t + 1] - lp[t]);
+      const fda::Level& L = H.levels[H.cubes[H.leaves[t]].level];
+      cost[t] = 100.0 * nt * src + 2.0 * (40.0 * nt * L.nsurf + 8.0 * L.s * L.nsurf);
+    }
+    // M2L flops per target cube (global cube id), spread over the cube's leaves by points
+    std::vector<double> cf(H.cubes.size(), 0.0);
+    for (const auto& g : H.m2l_groups) {
+      const fda::Level& L = H.levels[g.level];
+      const double f = g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s;
+      for (int64_t p = g.pbeg; p < g.pend; ++p) cf[L.cubes[L.in_cube[H.m2l_tgt[p]]]] += f;
+    }
+    for (int64_t t = 0; t < nl; ++t) {
+      const double nt = (double)(lp[t + 1] - lp[t]);
+      for (int64_t c = H.leaves[t]; c >= 0; c = H.cubes[c].parent)
+        if (cf[c] > 0) cost[t] += cf[c] * nt / (double)(H.cubes[c].pend - H.cubes[c].pbeg);
+    }
+    std::vector<double> pre(nl + 1, 0.0);
+    for (int64_t t = 0; t < nl; ++t) pre[t + 1] = pre[t] + cost[t];
+    for (int q = 1; q < R; ++q) {
+      const double target = pre[nl] * (double)q / (double)R;
+      rl[q] = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+      rl[q] = std::min(std::max(rl[q], rl[q - 1]), nl);
+    }
+  }
   P->nranks = R;
+  P->rank = r;
   P->nleaf = nl;
-  P->leaf_b = lb, P->leaf_e = le;
-  P->pt_b = lp[lb], P->pt_e = lp[le];
+  P->rank_leaf = rl;
+  P->rank_pt.assign(R + 1, 0);
+  for (int q = 0; q <= R; ++q) P->rank_pt[q] = lp[rl[q]];
+  P->leaf_b = rl[r], P->leaf_e = rl[r + 1];
+  P->pt_b = P->rank_pt[r], P->pt_e = P->rank_pt[r + 1];
   P->st.owned_begin = P->pt_b, P->st.owned_end = P->pt_e;
-  P->st.owned_leaf_begin = lb, P->st.owned_leaf_end = le;
+  P->st.owned_leaf_begin = P->leaf_b, P->st.owned_leaf_end = P->leaf_e;
   P->st.n = n;
   P->st.nleaves = nl;
   P->st.nlevels = (int64_t)H.levels.size();
   P->st.lmin = H.lmin;
 }
+
+// does the cube (global id) contain points of rank q?
+inline bool cube_on_rank(fda_plan P, int64_t gid, int q) {
+  const fda::Cube& c = P->H.cubes[gid];
+  return P->rank_pt[q] < P->rank_pt[q + 1] && c.pend > P->rank_pt[q] && c.pbeg < P->rank_pt[q + 1];
+}
+// ranks [*a, *b] whose point ranges meet the cube (empty ranks inside the interval are skipped by callers)
+inline void cube_ranks(fda_plan P, int64_t gid, int* a, int* b) {
+  const fda::Cube& c = P->H.cubes[gid];
+  *a = (int)(std::upper_bound(P->rank_pt.begin(), P->rank_pt.end(), c.pbeg) - P->rank_pt.begin()) - 1;
+  *b = (int)(std::upper_bound(P->rank_pt.begin(), P->rank_pt.end(), c.pend - 1) - P->rank_pt.begin()) - 1;
+  *a = std::min(std::max(*a, 0), P->nranks - 1);
+  *b = std::min(std::max(*b, 0), P->nranks - 1);
+}
+
+// Exchange lists.  Every rank runs S2M on its own leaves and M2M on the cubes that contain
+// its points, so its outgoing expansion of a cube is the partial sum over its own points (M2M is linear);
+// the full expansion is the sum of the partials of the cube's ranks.  Rank q needs the full expansion of
+// every source slot of an M2L pair whose target cube contains points of q.  So rank r sends its partial of
+// slot s to every q != r that needs s, and receives from every other rank of cube(s) the slots it needs.
+// Both sides enumerate (level, slot) in ascending order, so the lists agree without negotiation.
+void build_exchange(fda_plan P) {
+  const fda::HostPlan& H = P->H;
+  const int R = P->nranks, r = P->rank;
+  auto& X = P->xc;
+  X.send.assign(R, {});
+  X.recv.assign(R, {});
+  if (R == 1) return;
+  const int nlev = (int)H.levels.size();
+  std::vector<std::vector<int64_t>> grp_by_level(nlev);
+  for (size_t g = 0; g < H.m2l_groups.size(); ++g) grp_by_level[H.m2l_groups[g].level].push_back((int64_t)g);
+  for (int l = 0; l < nlev; ++l) {
+    const fda::Level& L = H.levels[l];
+    if (grp_by_level[l].empty() || L.n_out == 0) continue;
+    // need[s]: bit q set iff rank q needs out slot s (R <= 64)
+    std::vector<uint64_t> need(L.n_out, 0);
+    std::vector<uint64_t> tmask(L.n_in, 0);
+    for (int64_t t = 0; t < L.n_in; ++t) {
+      const int64_t gid = L.cubes[L.in_cube[t]];
+      int a, b;
+      cube_ranks(P, gid, &a, &b);
+      for (int q = a; q <= b; ++q)
+        if (cube_on_rank(P, gid, q)) tmask[t] |= 1ull << q;
+    }
+    for (int64_t g : grp_by_level[l]) {
+      const auto& G = H.m2l_groups[g];
+      for (int64_t p = G.pbeg; p < G.pend; ++p) need[H.m2l_src[p]] |= tmask[H.m2l_tgt[p]];
+    }
+    for (int64_t s = 0; s < L.n_out; ++s) {
+      if (!need[s]) continue;
+      const int64_t gid = L.cubes[L.out_cube[s]];
+      int a, b;
+      cube_ranks(P, gid, &a, &b);
+      if (cube_on_rank(P, gid, r))
+        for (int q = 0; q < R; ++q)
+          if (q != r && ((need[s] >> q) & 1)) X.send[q].push_back({l, s});
+      if ((need[s] >> r) & 1)
+        for (int q = a; q <= b; ++q)
+          if (q != r && cube_on_rank(P, gid, q)) X.recv[q].push_back({l, s});
+    }
+  }
+  X.send_cnt.assign(R, 0);
+  X.recv_cnt.assign(R, 0);
+  for (int q = 0; q < R; ++q) {
+    for (auto& e : X.send[q]) X.send_cnt[q] += H.levels[e.first].s;
+    for (auto& e : X.recv[q]) X.recv_cnt[q] += H.levels[e.first].s;
+    X.send_tot += X.send_cnt[q];
+    X.recv_tot += X.recv_cnt[q];
+  }
+  P->st.xchg_send_bytes = 16 * X.send_tot;
+  P->st.xchg_recv_bytes = 16 * X.recv_tot;
+}
+
+// device arrays of the exchange (after Xall / xoff exist)
+void upload_exchange(fda_plan P);
 
 fda_status upload_plan(fda_plan P, const fda_options& o) {
   fda::HostPlan& H = P->H;
@@ -385,18 +516,18 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   P->q = dalloc<double2>(P, n), P->phim = dalloc<double2>(P, n), P->outm = dalloc<double2>(P, n);
   P->phi_buf = dalloc<double2>(P, n), P->out_buf = dalloc<double2>(P, n);
   const int R = P->nranks;
-  auto owned_cube = [&](int64_t gid) {
-    const fda::Cube& c = H.cubes[gid];
-    return c.pend > P->pt_b && c.pbeg < P->pt_e;
-  };
-  // levels
+  auto owned_cube = [&](int64_t gid) { return R == 1 || cube_on_rank(P, gid, P->rank); };
+  // levels: all outgoing expansions in one allocation (the exchange addresses them by one offset)
   const int nlev = (int)H.levels.size();
   P->lv.assign(nlev, DevLevel());
+  P->xoff.assign(nlev + 1, 0);
+  for (int l = 0; l < nlev; ++l) P->xoff[l + 1] = P->xoff[l] + H.levels[l].n_out * (int64_t)H.levels[l].s;
+  if (P->xoff[nlev]) P->Xall = dalloc<double2>(P, (size_t)P->xoff[nlev]);
   for (int l = 0; l < nlev; ++l) {
     const fda::Level& L = H.levels[l];
     DevLevel& D = P->lv[l];
     D.s = L.s, D.n_out = L.n_out, D.n_in = L.n_in;
-    if (L.n_out) D.X = dalloc<double2>(P, (size_t)L.n_out * L.s);
+    if (L.n_out) D.X = P->Xall + P->xoff[l];
     if (L.n_in) D.Y = dalloc<double2>(P, (size_t)L.n_in * L.s);
   }
   // M2L: pairs filtered to owned targets, grouped by offset, split into owned work items
@@ -420,7 +551,9 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->st.m2l_pairs += (int64_t)np;
       P->st.m2l_groups += 1;
       P->st.m2l_lowrank_groups += g.rank >= 0;
-      P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s);
+      // algorithmic flops with the wedges' own expansion lengths (the pool pads them to the level's max)
+      const double ss = L.sdir(g.dir), st_ = L.sdir(L.hf ? fda::anti_dir(g.dir, L.m) : 0);
+      P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * st_ * ss : 8.0 * g.rank * (st_ + ss));
     }
     if (G.out.empty()) continue;
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
@@ -449,18 +582,21 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const fda::Level& Lc = H.levels[T.lp + 1];
     D.lp = T.lp, D.sp = T.sp, D.sc = T.sc;
     const int64_t nmat = (int64_t)(T.pool.size() / std::max<size_t>(1, (size_t)T.sp * T.sc));
+    // CSR by output slot -> group-major pairs, keeping the pairs keep(out slot, in slot) accepts
     auto grouped = [&](const std::vector<int64_t>& ptr, const std::vector<int64_t>& other,
-                       const std::vector<int64_t>& mat) {
-      // CSR by output slot -> group-major pairs
+                       const std::vector<int64_t>& mat, auto keep) {
       GroupedPairs G;
       std::vector<int64_t> cnt(nmat + 1, 0);
-      for (int64_t m : mat) cnt[T.mat_index[m] + 1]++;
+      for (int64_t s = 0; s + 1 < (int64_t)ptr.size(); ++s)
+        for (int64_t e = ptr[s]; e < ptr[s + 1]; ++e)
+          if (keep(s, other[e])) cnt[T.mat_index[mat[e]] + 1]++;
       for (int64_t g = 0; g < nmat; ++g) cnt[g + 1] += cnt[g];
-      G.out.assign(other.size(), 0);
-      G.in.assign(other.size(), 0);
+      G.out.assign(cnt[nmat], 0);
+      G.in.assign(cnt[nmat], 0);
       std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
       for (int64_t s = 0; s + 1 < (int64_t)ptr.size(); ++s)
         for (int64_t e = ptr[s]; e < ptr[s + 1]; ++e) {
+          if (!keep(s, other[e])) continue;
           const int64_t pos = fill[T.mat_index[mat[e]]]++;
           G.out[pos] = s;
           G.in[pos] = other[e];
@@ -472,44 +608,56 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       }
       return G;
     };
+    // multi-GPU: M2M only from child cubes with points of this rank (partial sums); L2L only
+    // into child cubes with points of this rank (their local expansions are complete here)
+    double fup = 0, fdn = 0;  // algorithmic flops with the directions' own expansion lengths
+    auto up_keep = [&](int64_t ps, int64_t cs) {
+      if (!owned_cube(Lc.cubes[Lc.out_cube[cs]])) return false;
+      fup += 8.0 * Lp.sdir(Lp.out_dir[ps]) * Lc.sdir(Lc.out_dir[cs]);
+      return true;
+    };
+    auto dn_keep = [&](int64_t cs, int64_t ps) {
+      if (!owned_cube(Lc.cubes[Lc.in_cube[cs]])) return false;
+      fdn += 8.0 * Lp.sdir(Lp.in_dir[ps]) * Lc.sdir(Lc.in_dir[cs]);
+      return true;
+    };
     if (!T.up_child.empty()) {
-      GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat);
+      GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat, up_keep);
       D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc, T.pool.data());
     }
     if (!T.dn_parent.empty()) {
-      GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat);
+      GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat, dn_keep);
       D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp, T.poolT.data());
     }
-    P->st.flops_m2m += 8.0 * T.sp * T.sc * (double)T.up_child.size();
-    P->st.flops_l2l += 8.0 * T.sp * T.sc * (double)T.dn_parent.size();
+    P->st.flops_m2m += 0.5 * fup;  // keep() runs twice per pair (count, fill)
+    P->st.flops_l2l += 0.5 * fdn;
     P->tr.push_back(D);
   }
-  // leaf operators
+  // leaf operators: S2M and L2T on this rank's leaves
   for (const auto& O : H.leafops) {
     const fda::Level& L = H.levels[O.level];
     DevLeafOps D;
     D.level = O.level, D.s = L.s, D.nsurf = L.nsurf;
-    D.nleaves = (int64_t)O.leaf.size();
-    D.leaf = upload_i32(P, O.leaf);
     std::vector<int64_t> lo_, so_;
     for (size_t t = 0; t < O.leaf.size(); ++t)
       if (O.leaf[t] >= P->leaf_b && O.leaf[t] < P->leaf_e) lo_.push_back(O.leaf[t]), so_.push_back(O.slot[t]);
     D.nleaves_own = (int64_t)lo_.size();
+    if (lo_.empty()) continue;
     D.leaf_own = upload_i32(P, lo_);
     std::vector<double> sf;
     for (const auto& p : L.ck_pts) sf.insert(sf.end(), {p[0], p[1], p[2]});
     D.surf = upload(P, sf);
-    {  // S2M reduction: pairs (out = leaf slot, in = leaf row t of the check-potential buffer)
+    {  // S2M reduction: pairs (out = leaf slot, in = owned-leaf row t of the check-potential buffer)
       GroupedPairs G;
-      G.out = O.slot;
-      G.in.resize(O.leaf.size());
-      for (size_t t = 0; t < O.leaf.size(); ++t) G.in[t] = (int64_t)t;
+      G.out = so_;
+      G.in.resize(lo_.size());
+      for (size_t t = 0; t < lo_.size(); ++t) G.in[t] = (int64_t)t;
       G.gptr.push_back((int64_t)G.out.size());
       G.rank.push_back(-1);
       G.mat.push_back(0);
       D.s2m = make_items(P, G, L.out_cube, L.out_dir, (int64_t)L.cubes.size(), L.s, L.nsurf, O.S.data());
     }
-    if (!lo_.empty()) {  // L2T reduction: pairs (out = owned leaf row t', in = leaf slot)
+    {  // L2T reduction: pairs (out = owned-leaf row t, in = leaf slot)
       GroupedPairs G;
       G.in = so_;
       G.out.resize(lo_.size());
@@ -521,18 +669,25 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       G.mat.push_back(0);
       D.l2t = make_items(P, G, oc, od, (int64_t)L.cubes.size(), L.nsurf, L.s, O.T.data());
     }
-    P->surfbuf_n = std::max(P->surfbuf_n, (int64_t)O.leaf.size() * L.nsurf);
-    for (int64_t t = 0; t < D.nleaves; ++t) {
-      const double npt = (double)(lp[O.leaf[t] + 1] - lp[O.leaf[t]]);
-      P->st.flops_s2m += npt * L.nsurf * 40.0 + 8.0 * L.s * L.nsurf;
-    }
+    P->surfbuf_n = std::max(P->surfbuf_n, (int64_t)lo_.size() * L.nsurf);
     for (size_t t = 0; t < lo_.size(); ++t) {
-      const double npt = (double)(lp[lo_[t] + 1] - lp[lo_[t]]);
-      P->st.flops_l2t += npt * L.nsurf * 45.0 + 8.0 * L.s * L.nsurf;
+      const int64_t npt = lp[lo_[t] + 1] - lp[lo_[t]];
+      P->st.s2m_evals += npt * L.nsurf;
+      P->st.l2t_evals += npt * L.nsurf;
+      P->st.flops_s2m += 8.0 * L.s * L.nsurf;  // the reduction x~ = S chk (eq_cmps); the evaluations are counted apart
+      P->st.flops_l2t += 8.0 * L.s * L.nsurf;
     }
     P->lo.push_back(D);
   }
   if (P->surfbuf_n) P->surfbuf = dalloc<double2>(P, (size_t)P->surfbuf_n);
+  // every translation launch must fit the device's shared memory (large expansions at small eps)
+  {
+    bool fits = true;
+    for (const auto& D : P->lv) fits &= fda::gtrans_fits(D.m2l) && fda::gtrans_fits(D.m2l2);
+    for (const auto& T : P->tr) fits &= fda::gtrans_fits(T.up) && fda::gtrans_fits(T.dn);
+    for (const auto& O : P->lo) fits &= fda::gtrans_fits(O.s2m) && fda::gtrans_fits(O.l2t);
+    if (!fits) return FDA_ERR_SETUP_ACCURACY;
+  }
   // stats
   fda_stats& s = P->st;
   s.n = n;
@@ -543,11 +698,57 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   for (int64_t t = P->leaf_b; t < P->leaf_e; ++t)
     for (int64_t e = H.p2p_ptr[t]; e < H.p2p_ptr[t + 1]; ++e)
       s.p2p_point_pairs += (lp[t + 1] - lp[t]) * (lp[H.p2p_src[e] + 1] - lp[H.p2p_src[e]]);
-  s.flops_p2p = 100.0 * (double)s.p2p_point_pairs;
+  const int kk = std::min(std::max(P->kind, 0), 2);
+  s.flops_p2p = FLOP_P2P[kk] * (double)s.p2p_point_pairs;
+  s.flops_s2m += FLOP_S2M[kk] * (double)s.s2m_evals;
+  s.flops_l2t += FLOP_L2T * (double)s.l2t_evals;
   for (int l = 0; l < nlev; ++l) s.out_slots += H.levels[l].n_out, s.in_slots += H.levels[l].n_in;
   s.owned_begin = P->pt_b, s.owned_end = P->pt_e;
   s.setup_tree_s = H.t_tree, s.setup_lists_s = H.t_lists, s.setup_ops_s = H.t_ops;
+  upload_exchange(P);
   return FDA_OK;
+}
+
+void upload_exchange(fda_plan P) {
+  auto& X = P->xc;
+  const int R = P->nranks;
+  if (R == 1) return;
+  const fda::HostPlan& H = P->H;
+  std::vector<int64_t> sx, sb;
+  std::vector<int32_t> sl;
+  int64_t off = 0;
+  for (int q = 0; q < R; ++q)
+    for (auto& e : X.send[q]) {
+      const int s_ = H.levels[e.first].s;
+      sx.push_back(P->xoff[e.first] + e.second * s_), sl.push_back(s_), sb.push_back(off);
+      off += s_;
+    }
+  X.nsend = (int64_t)sx.size();
+  // received entries grouped by destination (level, slot), partials in peer order
+  std::vector<std::pair<std::pair<int, int64_t>, std::pair<int, int64_t>>> rv;  // ((level, slot), (peer, buf off))
+  off = 0;
+  for (int q = 0; q < R; ++q)
+    for (auto& e : X.recv[q]) {
+      rv.push_back({e, {q, off}});
+      off += H.levels[e.first].s;
+    }
+  std::stable_sort(rv.begin(), rv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<int64_t> dx, dp{0}, ro;
+  std::vector<int32_t> dl;
+  for (size_t i = 0; i < rv.size(); ++i) {
+    if (i == 0 || rv[i].first != rv[i - 1].first) {
+      if (i) dp.push_back((int64_t)ro.size());
+      const int s_ = H.levels[rv[i].first.first].s;
+      dx.push_back(P->xoff[rv[i].first.first] + rv[i].first.second * s_), dl.push_back(s_);
+    }
+    ro.push_back(rv[i].second.second);
+  }
+  if (!rv.empty()) dp.push_back((int64_t)ro.size());
+  X.ndst = (int64_t)dx.size();
+  X.s_xoff = upload(P, sx), X.s_len = upload(P, sl), X.s_boff = upload(P, sb);
+  X.d_xoff = upload(P, dx), X.d_len = upload(P, dl), X.d_rptr = upload(P, dp), X.d_roff = upload(P, ro);
+  X.sendbuf = dalloc<double2>(P, (size_t)std::max<int64_t>(1, X.send_tot));
+  X.recvbuf = dalloc<double2>(P, (size_t)std::max<int64_t>(1, X.recv_tot));
 }
 
 bool finite3(const std::vector<double>& v) {
@@ -566,8 +767,8 @@ void fda_options_default(fda_options* o) {
   fda::Options d;
   o->leaf_size = 0;
   o->eps_internal = 0;
-  o->lf_p_low = d.lf_p_low;
-  o->lf_p_high = d.lf_p_high;
+  o->lf_p_low = 0;  // eps-dependent default
+  o->lf_p_high = 0;
   o->lf_p_switch = d.lf_p_switch;
   o->lowrank = 1;
   o->single_leaf = 0;
@@ -606,6 +807,8 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
   fda_options o;
   fda_options_default(&o);
   if (opt) o = *opt;
+  if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG && o.kernel != FDA_KERNEL_T1) return FDA_ERR_INVALID_ARG;
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return FDA_ERR_INVALID_ARG;
   int ndev = 0;
   if (!o.host_only && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)) {
     cudaGetLastError();
@@ -625,8 +828,8 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     fo.np = o.leaf_size;
     fo.eps_int = o.eps_internal;
     fo.eps_lr = o.eps_lowrank;
-    if (o.lf_p_low > 1) fo.lf_p_low = o.lf_p_low;
-    if (o.lf_p_high > 1) fo.lf_p_high = o.lf_p_high;
+    fo.lf_p_low = o.lf_p_low > 1 ? o.lf_p_low : 0;  // 0: the eps-dependent default (plan.cpp, R17)
+    fo.lf_p_high = o.lf_p_high > 1 ? o.lf_p_high : 0;
     if (o.lf_p_switch > 0) fo.lf_p_switch = o.lf_p_switch;
     fo.lowrank = o.lowrank;
     fo.single_leaf = o.single_leaf;
@@ -638,9 +841,9 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     if (!err.empty()) return FDA_ERR_INVALID_ARG;
     P->host_only = o.host_only != 0;
     P->logstr = P->H.log;
-    set_ownership(P.get(), o);
-    if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG && o.kernel != FDA_KERNEL_T1) return FDA_ERR_INVALID_ARG;
     P->kind = o.kernel;
+    set_ownership(P.get(), o);
+    build_exchange(P.get());
     if (P->host_only) {
       *out = P.release();
       return FDA_OK;
@@ -689,50 +892,59 @@ fda_status fda_plan_set_correction(fda_plan P, int64_t nnz, const int64_t* row_p
   if (nnz < 0) return FDA_ERR_INVALID_ARG;
   if (nnz > 0 && (!row_ptr || !col || !val)) return FDA_ERR_INVALID_ARG;
   try {
-    if (P->c_ptr) {
-      // release the old correction
+    const int64_t n = P->n;
+    int64_t* n_ptr = nullptr;
+    int32_t* n_col = nullptr;
+    double2* n_val = nullptr;
+    int64_t own = 0;
+    if (nnz > 0) {
+      // validate and permute into NEW buffers first: on any error the plan keeps its current correction
+      std::vector<int64_t> rp = to_host(row_ptr, (size_t)n + 1);
+      if (rp[0] != 0 || rp[n] != nnz) return FDA_ERR_INVALID_ARG;
+      for (int64_t i = 0; i < n; ++i)
+        if (rp[i + 1] < rp[i]) return FDA_ERR_INVALID_ARG;
+      std::vector<int32_t> cl = to_host(col, (size_t)nnz);
+      for (int64_t p = 0; p < nnz; ++p)
+        if (cl[p] < 0 || cl[p] >= n) return FDA_ERR_INVALID_ARG;
+      std::vector<double> vl = to_host(val, (size_t)nnz * 2);
+      // permute into Morton order: row m = caller row perm[m]; columns through the inverse permutation
+      const std::vector<int32_t>& perm = P->H.perm;
+      std::vector<int32_t> inv(n);
+      for (int64_t m = 0; m < n; ++m) inv[perm[m]] = (int32_t)m;
+      std::vector<int64_t> mp(n + 1, 0);
+      for (int64_t m = 0; m < n; ++m) mp[m + 1] = mp[m] + (rp[perm[m] + 1] - rp[perm[m]]);
+      // only this rank's rows are stored (a multi-GPU rank applies its own rows)
+      const int64_t o0 = mp[P->pt_b], o1 = mp[P->pt_e];
+      std::vector<int32_t> mc(o1 - o0);
+      std::vector<double> mv((size_t)(o1 - o0) * 2);
+#pragma omp parallel for schedule(dynamic, 1024)
+      for (int64_t m = P->pt_b; m < P->pt_e; ++m) {
+        const int64_t i = perm[m];
+        int64_t o = mp[m] - o0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p, ++o) {
+          mc[o] = inv[cl[p]];
+          mv[2 * o] = vl[2 * p];
+          mv[2 * o + 1] = vl[2 * p + 1];
+        }
+      }
+      std::vector<double>().swap(vl);
+      for (auto& v : mp) v -= o0;
+      n_ptr = upload(P, mp);
+      n_col = upload(P, mc);
+      n_val = upload(P, reinterpret_cast<const double2*>(mv.data()), (size_t)(o1 - o0));
+      own = o1 - o0;
+    }
+    if (P->c_ptr) {  // release the old correction only now that the new one is in place
       for (void* p : {(void*)P->c_ptr, (void*)P->c_col, (void*)P->c_val}) {
         auto it = std::find(P->allocs.begin(), P->allocs.end(), p);
         if (it != P->allocs.end()) P->allocs.erase(it);
         cudaFree(p);
       }
-      P->c_ptr = nullptr, P->c_col = nullptr, P->c_val = nullptr, P->nnz = 0;
     }
-    if (nnz == 0) return FDA_OK;
-    const int64_t n = P->n;
-    std::vector<int64_t> rp = to_host(row_ptr, (size_t)n + 1);
-    if (rp[0] != 0 || rp[n] != nnz) return FDA_ERR_INVALID_ARG;
-    for (int64_t i = 0; i < n; ++i)
-      if (rp[i + 1] < rp[i]) return FDA_ERR_INVALID_ARG;
-    std::vector<int32_t> cl = to_host(col, (size_t)nnz);
-    for (int64_t p = 0; p < nnz; ++p)
-      if (cl[p] < 0 || cl[p] >= n) return FDA_ERR_INVALID_ARG;
-    std::vector<double> vl = to_host(val, (size_t)nnz * 2);
-    // permute into Morton order: row m = caller row perm[m]; columns through the inverse permutation
-    const std::vector<int32_t>& perm = P->H.perm;
-    std::vector<int32_t> inv(n);
-    for (int64_t m = 0; m < n; ++m) inv[perm[m]] = (int32_t)m;
-    std::vector<int64_t> mp(n + 1, 0);
-    for (int64_t m = 0; m < n; ++m) mp[m + 1] = mp[m] + (rp[perm[m] + 1] - rp[perm[m]]);
-    std::vector<int32_t> mc(nnz);
-    std::vector<double> mv((size_t)nnz * 2);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t m = 0; m < n; ++m) {
-      const int64_t i = perm[m];
-      int64_t o = mp[m];
-      for (int64_t p = rp[i]; p < rp[i + 1]; ++p, ++o) {
-        mc[o] = inv[cl[p]];
-        mv[2 * o] = vl[2 * p];
-        mv[2 * o + 1] = vl[2 * p + 1];
-      }
-    }
-    P->c_ptr = upload(P, mp);
-    P->c_col = upload(P, mc);
-    P->c_val = upload(P, reinterpret_cast<const double2*>(mv.data()), (size_t)nnz);
+    P->c_ptr = n_ptr, P->c_col = n_col, P->c_val = n_val;
     P->nnz = nnz;
     P->st.csr_nnz = nnz;
-    int64_t own = mp[P->pt_e] - mp[P->pt_b];
-    P->st.bytes_csr = 20.0 * (double)own + 48.0 * (double)(P->pt_e - P->pt_b);
+    P->st.bytes_csr = nnz ? 20.0 * (double)own + 48.0 * (double)(P->pt_e - P->pt_b) : 0.0;
     P->st.device_bytes = P->bytes;
   } catch (const CudaFail& f) {
     P->sticky_error = true;
@@ -743,127 +955,244 @@ fda_status fda_plan_set_correction(fda_plan P, int64_t nnz, const int64_t* row_p
   return FDA_OK;
 }
 
-static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, double* out, float* phase_ms) {
+}  // extern "C"
+
+// ---------------------------------------------------------------- apply
+// Phases (fda_apply_timed indices): 0 permute, 1 p2p, 2 csr, 3 s2m, 4 m2m, 5 m2l, 6 l2l, 7 l2t, 8 unpermute,
+// 9 exchange.  The stages below are stream-ordered on st; none synchronises the host.
+namespace {
+
+struct Marks {
+  cudaEvent_t ev[2 * FDA_NPHASES] = {};
+  bool on = false;
+  cudaStream_t st = 0;
+  void begin(int ph) {
+    if (on) ck(cudaEventRecord(ev[2 * ph], st));
+  }
+  void end(int ph) {
+    if (on) ck(cudaEventRecord(ev[2 * ph + 1], st));
+  }
+};
+
+// FDA_TRACE=1: synchronise after every far-field launch and print its wall time (diagnostics only)
+struct Trace {
+  bool on = getenv("FDA_TRACE") != nullptr;
+  double t = now();
+  void operator()(cudaStream_t st, const char* what, int l) {
+    if (!on) return;
+    ck(cudaStreamSynchronize(st));
+    const double t1 = now();
+    fprintf(stderr, "[fda trace] %-4s level %d  %.3f ms\n", what, l, 1e3 * (t1 - t));
+    t = t1;
+  }
+};
+
+fda::Points points_of(fda_plan P) { return fda::Points{P->px, P->py, P->pz, P->nx, P->ny, P->nz, P->w}; }
+fda::LeafGeom leaves_of(fda_plan P) { return fda::LeafGeom{P->leaf_ptr, P->lcx, P->lcy, P->lcz}; }
+double2 alpha_of(fda_plan P) { return make_double2(P->H.alpha.real(), P->H.alpha.imag()); }
+bool has_far(fda_plan P, uint32_t mask) { return (mask & FDA_PHASE_FAR) && P->H.lmin >= 0; }
+
+// H1 + upward pass (H4 S2M on this rank's leaves, H5 M2M on cubes with this rank's points) + pack of the
+// partial expansions other ranks need into sendbuf
+void stage_up(fda_plan P, uint32_t mask, const double2* d_phi, double2* sendbuf, cudaStream_t st, Marks& mk,
+              Trace& tr) {
+  const fda::Points Pt = points_of(P);
+  const fda::LeafGeom Lg = leaves_of(P);
+  mk.begin(0);
+  fda::launch_permute_scale(P->n, P->perm, P->w, d_phi, P->q, P->phim, st);
+  mk.end(0);
+  if (!has_far(P, mask)) return;
+  mk.begin(3);
+  // M2M accumulates into the non-leaf slots: clear every level's outgoing expansions first
+  if (P->xoff.back()) ck(cudaMemsetAsync(P->Xall, 0, (size_t)P->xoff.back() * sizeof(double2), st));
+  for (const auto& O : P->lo) {
+    fda::launch_s2m_check(P->kind, O.nleaves_own, O.leaf_own, Lg, Pt, P->q, O.surf, O.nsurf, P->H.k, alpha_of(P),
+                          P->surfbuf, st);
+    ck(fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st));
+    tr(st, "s2m", O.level);
+  }
+  mk.end(3);
+  mk.begin(4);
+  for (int t = (int)P->tr.size() - 1; t >= 0; --t) {
+    const DevTrans& T = P->tr[t];
+    ck(fda::launch_gtrans(T.up, P->lv[T.lp + 1].X, P->lv[T.lp].X, st));
+    tr(st, "m2m", T.lp);
+  }
+  if (P->nranks > 1)
+    fda::launch_xpack(P->xc.nsend, P->xc.s_xoff, P->xc.s_len, P->xc.s_boff, P->Xall, sendbuf, st);
+  mk.end(4);
+}
+
+// H2 P2P + H3 correction on this rank's rows (outm of the other rows is cleared when they are not computed)
+void stage_near(fda_plan P, uint32_t mask, cudaStream_t st, Marks& mk) {
+  const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
+  mk.begin(1);
+  if (!(mask & FDA_PHASE_NEAR) || partial) ck(cudaMemsetAsync(P->outm, 0, (size_t)P->n * sizeof(double2), st));
+  if (mask & FDA_PHASE_NEAR)
+    fda::launch_p2p(P->kind, P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, points_of(P), P->q, P->H.k,
+                    alpha_of(P), P->outm, P->leaf_b, st);
+  mk.end(1);
+  mk.begin(2);
+  if ((mask & FDA_PHASE_CORR) && P->nnz > 0)
+    fda::launch_csr(P->pt_b, P->pt_e, P->c_ptr, P->c_col, P->c_val, P->phim, P->outm, st);
+  mk.end(2);
+}
+
+// unpack of the received partial expansions, then H6 M2L, H7 L2L, H8 L2T into this rank's rows
+void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t st, Marks& mk, Trace& tr) {
+  if (!has_far(P, mask)) return;
+  const fda::Points Pt = points_of(P);
+  const fda::LeafGeom Lg = leaves_of(P);
+  mk.begin(5);
+  if (P->nranks > 1)
+    fda::launch_xunpack(P->xc.ndst, P->xc.d_xoff, P->xc.d_len, P->xc.d_rptr, P->xc.d_roff, recvbuf, P->Xall, st);
+  for (auto& D : P->lv)
+    if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
+  for (size_t l = 0; l < P->lv.size(); ++l) {
+    ck(fda::launch_gtrans(P->lv[l].m2l, P->lv[l].X, P->lv[l].Y, st));
+    ck(fda::launch_gtrans(P->lv[l].m2l2, P->lv[l].X, P->lv[l].Y, st));
+    if (P->lv[l].m2l.n_items) tr(st, "m2l", (int)l);
+  }
+  mk.end(5);
+  mk.begin(6);
+  for (const auto& T : P->tr) {
+    ck(fda::launch_gtrans(T.dn, P->lv[T.lp].Y, P->lv[T.lp + 1].Y, st));
+    tr(st, "l2l", T.lp);
+  }
+  mk.end(6);
+  mk.begin(7);
+  for (const auto& O : P->lo) {
+    ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
+    ck(fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st));
+    // E_dn = G + alpha dG/dn_x (BM_H, BM_G: PAPER.md eq_eval2t); the Table-1 kernel has no target
+    // derivative: E_dn = G
+    const double2 alpha_dn = P->kind == FDA_KERNEL_T1 ? make_double2(0.0, 0.0) : alpha_of(P);
+    fda::launch_l2t_eval(O.nleaves_own, O.leaf_own, Lg, Pt, O.surf, O.nsurf, P->H.k, alpha_dn, P->surfbuf, P->outm,
+                         st);
+    tr(st, "l2t", O.level);
+  }
+  mk.end(7);
+}
+
+// kernels one apply launches (memsets excluded)
+int64_t count_launches(fda_plan P, uint32_t mask) {
+  int64_t L = 3;  // permute, p2p, unpermute
+  if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
+  if (has_far(P, mask)) {
+    for (const auto& O : P->lo) L += 4 * (O.nleaves_own > 0);
+    for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
+    for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0);
+    if (P->nranks > 1) L += (P->xc.nsend > 0) + (P->xc.ndst > 0);
+  }
+  return L;
+}
+
+// multi-GPU exchange over NCCL: grouped send / receive of the partial expansions with every peer
+void nccl_exchange(fda_plan P, cudaStream_t st) {
+  const fda::Nccl& N = fda::nccl();
+  auto& X = P->xc;
+  auto nck = [](ncclResult_t r) {
+    if (r != ncclSuccess) throw CudaFail{FDA_ERR_NCCL};
+  };
+  nck(N.GroupStart());
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < P->nranks; ++q) {
+    if (X.send_cnt[q]) nck(N.Send(X.sendbuf + so, 2 * (size_t)X.send_cnt[q], ncclDouble, q, P->comm, st));
+    if (X.recv_cnt[q]) nck(N.Recv(X.recvbuf + ro, 2 * (size_t)X.recv_cnt[q], ncclDouble, q, P->comm, st));
+    so += X.send_cnt[q], ro += X.recv_cnt[q];
+  }
+  nck(N.GroupEnd());
+}
+// multi-GPU output assembly: every rank broadcasts its own (contiguous, Morton-order) rows of outm
+void nccl_allgather_out(fda_plan P, cudaStream_t st) {
+  const fda::Nccl& N = fda::nccl();
+  auto nck = [](ncclResult_t r) {
+    if (r != ncclSuccess) throw CudaFail{FDA_ERR_NCCL};
+  };
+  nck(N.GroupStart());
+  for (int q = 0; q < P->nranks; ++q) {
+    const int64_t b = P->rank_pt[q], e = P->rank_pt[q + 1];
+    if (e > b) nck(N.Broadcast(P->outm + b, P->outm + b, 2 * (size_t)(e - b), ncclDouble, q, P->comm, st));
+  }
+  nck(N.GroupEnd());
+}
+
+fda_status check_apply_args(fda_plan P, const void* phi, const void* out) {
   if (!P || !phi || !out) return FDA_ERR_INVALID_ARG;
   if (P->host_only) return FDA_ERR_STATE;
   if (P->sticky_error) return FDA_ERR_CUDA;
-  if ((const void*)phi == (const void*)out) return FDA_ERR_ALIAS;
+  if (phi == out) return FDA_ERR_ALIAS;
+  return FDA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, double* out, float* phase_ms) {
+  fda_status cs = check_apply_args(P, phi, out);
+  if (cs != FDA_OK) return cs;
+  // a partitioned plan without a communicator computes only its own rows and needs the expansions of the
+  // other ranks: it is driven through fda_apply_up / fda_apply_down
+  if (P->nranks > 1 && !P->comm) return FDA_ERR_STATE;
   const int64_t n = P->n;
   cudaStream_t st = P->stream;
   const bool dphi = is_device_ptr(phi), dout = is_device_ptr(out);
   if (phase_ms && (!dphi || !dout)) return FDA_ERR_INVALID_ARG;
+  Marks mk;
+  mk.st = st;
+  mk.on = phase_ms != nullptr;
   try {
     const double2* d_phi = reinterpret_cast<const double2*>(phi);
     double2* d_out = reinterpret_cast<double2*>(out);
     if (!dphi) {
       ck(cudaMemcpyAsync(P->phi_buf, phi, (size_t)n * sizeof(double2), cudaMemcpyHostToDevice, st));
+      // pinned host memory makes the copy asynchronous: the caller may reuse phi once we return, so wait
+      // for it here when nothing below synchronises (device output)
+      if (dout) ck(cudaStreamSynchronize(st));
       d_phi = P->phi_buf;
     }
     if (!dout) d_out = P->out_buf;
-    cudaEvent_t ev[10];
-    if (phase_ms)
-      for (int i = 0; i < 10; ++i) ck(cudaEventCreate(&ev[i]));
-    auto mark = [&](int i) {
-      if (phase_ms) ck(cudaEventRecord(ev[i], st));
-    };
-    fda::Points Pt{P->px, P->py, P->pz, P->nx, P->ny, P->nz, P->w};
-    fda::LeafGeom Lg{P->leaf_ptr, P->lcx, P->lcy, P->lcz};
-    const double k = P->H.k;
-    const double2 alpha = make_double2(P->H.alpha.real(), P->H.alpha.imag());
-    mark(0);
-    fda::launch_permute_scale(n, P->perm, P->w, d_phi, P->q, P->phim, st);
-    mark(1);
-    const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
-    if (!(mask & FDA_PHASE_NEAR) || partial) ck(cudaMemsetAsync(P->outm, 0, (size_t)n * sizeof(double2), st));
-    if (mask & FDA_PHASE_NEAR)
-      fda::launch_p2p(P->kind, P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, Pt, P->q, k, alpha, P->outm,
-                      P->leaf_b, st);
-    mark(2);
-    if ((mask & FDA_PHASE_CORR) && P->nnz > 0)
-      fda::launch_csr(P->pt_b, P->pt_e, P->c_ptr, P->c_col, P->c_val, P->phim, P->outm, st);
-    mark(3);
-    const bool far = (mask & FDA_PHASE_FAR) && P->H.lmin >= 0;
-    // FDA_TRACE=1: synchronise after every far-field launch and print its wall time (diagnostics only)
-    static const bool trace = getenv("FDA_TRACE") != nullptr;
-    double tlast = now();
-    auto tr = [&](const char* what, int l) {
-      if (!trace) return;
-      ck(cudaStreamSynchronize(st));
-      const double t = now();
-      fprintf(stderr, "[fda trace] %-4s level %d  %.3f ms\n", what, l, 1e3 * (t - tlast));
-      tlast = t;
-    };
-    if (far) {
-      tr("pre", -1);
-      // M2M accumulates into the non-leaf slots: clear every level's outgoing expansions first
-      for (auto& D : P->lv)
-        if (D.n_out) ck(cudaMemsetAsync(D.X, 0, (size_t)D.n_out * D.s * sizeof(double2), st));
-      for (const auto& O : P->lo) {
-        fda::launch_s2m_check(P->kind, O.nleaves, O.leaf, Lg, Pt, P->q, O.surf, O.nsurf, k, alpha, P->surfbuf, st);
-        fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st);
-        tr("s2m", O.level);
-      }
+    if (mk.on)
+      for (auto& e : mk.ev) ck(cudaEventCreate(&e));
+    Trace tr;
+    stage_up(P, mask, d_phi, P->xc.sendbuf, st, mk, tr);
+    const bool xchg = P->nranks > 1 && has_far(P, mask);
+    if (xchg && !mk.on) {
+      // the exchange runs on the plan's side stream while P2P and the correction run here
+      ck(cudaEventRecord(P->ev_up, st));
+      ck(cudaStreamWaitEvent(P->xstream, P->ev_up, 0));
+      nccl_exchange(P, P->xstream);
+      ck(cudaEventRecord(P->ev_x, P->xstream));
+      stage_near(P, mask, st, mk);
+      ck(cudaStreamWaitEvent(st, P->ev_x, 0));
+    } else {
+      mk.begin(9);
+      if (xchg) nccl_exchange(P, st);
+      mk.end(9);
+      stage_near(P, mask, st, mk);
     }
-    mark(4);
-    if (far) {
-      for (int t = (int)P->tr.size() - 1; t >= 0; --t) {
-        const DevTrans& T = P->tr[t];
-        fda::launch_gtrans(T.up, P->lv[T.lp + 1].X, P->lv[T.lp].X, st);
-        tr("m2m", T.lp);
-      }
-    }
-    mark(5);
-    if (far) {
-      for (auto& D : P->lv)
-        if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
-      for (size_t l = 0; l < P->lv.size(); ++l) {
-        fda::launch_gtrans(P->lv[l].m2l, P->lv[l].X, P->lv[l].Y, st);
-        fda::launch_gtrans(P->lv[l].m2l2, P->lv[l].X, P->lv[l].Y, st);
-        if (P->lv[l].m2l.n_items) tr("m2l", (int)l);
-      }
-    }
-    mark(6);
-    if (far) {
-      for (const auto& T : P->tr) {
-        fda::launch_gtrans(T.dn, P->lv[T.lp].Y, P->lv[T.lp + 1].Y, st);
-        tr("l2l", T.lp);
-      }
-    }
-    mark(7);
-    if (far) {
-      for (const auto& O : P->lo) {
-        if (!O.nleaves_own) continue;
-        ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
-        fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st);
-        // E_dn = G + alpha dG/dn_x (BM_H, BM_G: PAPER.md eq_eval2t); the Table-1 kernel has no target
-        // derivative: E_dn = G
-        const double2 alpha_dn = P->kind == FDA_KERNEL_T1 ? make_double2(0.0, 0.0) : alpha;
-        fda::launch_l2t_eval(O.nleaves_own, O.leaf_own, Lg, Pt, O.surf, O.nsurf, k, alpha_dn, P->surfbuf, P->outm, st);
-        tr("l2t", O.level);
-      }
-    }
-    mark(8);
+    stage_down(P, mask, P->xc.recvbuf, st, mk, tr);
+    mk.begin(8);
+    if (P->comm) nccl_allgather_out(P, st);
     fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
-    mark(9);
+    mk.end(8);
     ck(cudaGetLastError());
-    {
-      int64_t L = 3;  // permute, p2p, unpermute
-      if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
-      if (far) {
-        for (const auto& O : P->lo) L += 2 * (O.nleaves > 0) + 2 * (O.nleaves_own > 0);
-        for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
-        for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0);
-      }
-      P->last_launches = L;
-    }
+    P->last_launches = count_launches(P, mask);
     if (!dout) {
       ck(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(double2), cudaMemcpyDeviceToHost, st));
       ck(cudaStreamSynchronize(st));
     }
-    if (phase_ms) {
-      ck(cudaEventSynchronize(ev[9]));
-      for (int i = 0; i < 9; ++i) ck(cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]));
-      for (int i = 0; i < 10; ++i) cudaEventDestroy(ev[i]);
+    if (mk.on) {
+      ck(cudaEventSynchronize(mk.ev[2 * 8 + 1]));
+      for (int i = 0; i < FDA_NPHASES; ++i) {
+        phase_ms[i] = 0.f;
+        if (cudaEventQuery(mk.ev[2 * i + 1]) == cudaSuccess &&
+            cudaEventElapsedTime(&phase_ms[i], mk.ev[2 * i], mk.ev[2 * i + 1]) != cudaSuccess)
+          phase_ms[i] = 0.f;
+      }
+      cudaGetLastError();
+      for (auto& e : mk.ev) cudaEventDestroy(e);
     }
   } catch (const CudaFail& f) {
     P->sticky_error = true;
@@ -879,6 +1208,56 @@ fda_status fda_apply_phases(fda_plan P, uint32_t mask, const double* phi, double
 fda_status fda_apply_timed(fda_plan P, uint32_t mask, const double* phi, double* out, float* phase_ms) {
   if (!phase_ms) return FDA_ERR_INVALID_ARG;
   return apply_impl(P, mask, phi, out, phase_ms);
+}
+
+fda_status fda_dist_counts(fda_plan P, int64_t* send_counts, int64_t* recv_counts) {
+  if (!P || !send_counts || !recv_counts) return FDA_ERR_INVALID_ARG;
+  for (int q = 0; q < P->nranks; ++q) {
+    send_counts[q] = P->nranks > 1 ? P->xc.send_cnt[q] : 0;
+    recv_counts[q] = P->nranks > 1 ? P->xc.recv_cnt[q] : 0;
+  }
+  return FDA_OK;
+}
+
+fda_status fda_apply_up(fda_plan P, const double* phi, double* sendbuf) {
+  if (!P || !phi) return FDA_ERR_INVALID_ARG;
+  if (P->host_only) return FDA_ERR_STATE;
+  if (P->sticky_error) return FDA_ERR_CUDA;
+  if (!is_device_ptr(phi) || (P->nranks > 1 && P->xc.send_tot > 0 && (!sendbuf || !is_device_ptr(sendbuf))))
+    return FDA_ERR_INVALID_ARG;
+  try {
+    Marks mk;
+    Trace tr;
+    stage_up(P, FDA_PHASE_ALL, reinterpret_cast<const double2*>(phi), reinterpret_cast<double2*>(sendbuf), P->stream,
+             mk, tr);
+    ck(cudaGetLastError());
+  } catch (const CudaFail& f) {
+    P->sticky_error = true;
+    return f.s;
+  }
+  return FDA_OK;
+}
+
+fda_status fda_apply_down(fda_plan P, const double* recvbuf, double* out) {
+  if (!P || !out) return FDA_ERR_INVALID_ARG;
+  if (P->host_only) return FDA_ERR_STATE;
+  if (P->sticky_error) return FDA_ERR_CUDA;
+  if (!is_device_ptr(out) || (P->nranks > 1 && P->xc.recv_tot > 0 && (!recvbuf || !is_device_ptr(recvbuf))))
+    return FDA_ERR_INVALID_ARG;
+  try {
+    Marks mk;
+    Trace tr;
+    cudaStream_t st = P->stream;
+    stage_near(P, FDA_PHASE_ALL, st, mk);
+    stage_down(P, FDA_PHASE_ALL, reinterpret_cast<const double2*>(recvbuf), st, mk, tr);
+    fda::launch_unpermute(P->n, P->perm, P->outm, reinterpret_cast<double2*>(out), st);
+    ck(cudaGetLastError());
+    P->last_launches = count_launches(P, FDA_PHASE_ALL);
+  } catch (const CudaFail& f) {
+    P->sticky_error = true;
+    return f.s;
+  }
+  return FDA_OK;
 }
 
 fda_status fda_plan_stats(fda_plan P, fda_stats* s) {
@@ -936,8 +1315,74 @@ fda_status fda_plan_export_m2l(fda_plan P, int64_t* npairs, int32_t* level, int6
   return FDA_OK;
 }
 
+fda_status fda_nccl_unique_id(char* id) {
+  if (!id) return FDA_ERR_INVALID_ARG;
+  const fda::Nccl& N = fda::nccl();
+  if (!N.ok) return FDA_ERR_NCCL;
+  ncclUniqueId u;
+  if (N.GetUniqueId(&u) != ncclSuccess) return FDA_ERR_NCCL;
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return FDA_OK;
+}
+
+fda_status fda_plan_create_dist(int64_t n, const double* points, const double* normals, const double* quad_weights,
+                                double k, double alpha_re, double alpha_im, double eps, const fda_options* opt,
+                                const char* nccl_id, int rank, int nranks, fda_plan* out) {
+  if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks || nranks > 64) return FDA_ERR_INVALID_ARG;
+  *out = nullptr;
+  fda_options o;
+  fda_options_default(&o);
+  if (opt) o = *opt;
+  if (o.host_only) return FDA_ERR_INVALID_ARG;
+  o.rank = rank, o.nranks = nranks;
+  const fda::Nccl& N = fda::nccl();
+  if (!N.ok) return FDA_ERR_NCCL;
+  fda_plan P = nullptr;
+  fda_status s = fda_plan_create_ex(n, points, normals, quad_weights, k, alpha_re, alpha_im, eps, &o, &P);
+  if (s != FDA_OK) return s;
+  ncclUniqueId u;
+  std::memcpy(u.internal, nccl_id, NCCL_UNIQUE_ID_BYTES);
+  if (N.CommInitRank(&P->comm, nranks, u, rank) != ncclSuccess) {
+    P->comm = nullptr;
+    fda_plan_destroy(P);
+    return FDA_ERR_NCCL;
+  }
+  if (cudaStreamCreateWithFlags(&P->xstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_up, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&P->ev_x, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    fda_plan_destroy(P);
+    return FDA_ERR_CUDA;
+  }
+  *out = P;
+  return FDA_OK;
+}
+
+fda_status fda_plan_export_exchange(fda_plan P, int peer, int recv, int64_t* count, int32_t* level, int64_t* slot,
+                                    int64_t* cube_ijk) {
+  if (!P || !count || peer < 0 || peer >= P->nranks) return FDA_ERR_INVALID_ARG;
+  if (P->nranks == 1) {
+    *count = 0;
+    return FDA_OK;
+  }
+  const auto& v = recv ? P->xc.recv[peer] : P->xc.send[peer];
+  *count = (int64_t)v.size();
+  for (size_t i = 0; i < v.size(); ++i) {
+    const fda::Level& L = P->H.levels[v[i].first];
+    if (level) level[i] = v[i].first;
+    if (slot) slot[i] = v[i].second;
+    if (cube_ijk)
+      for (int d = 0; d < 3; ++d) cube_ijk[3 * i + d] = P->H.cubes[L.cubes[L.out_cube[v[i].second]]].ijk[d];
+  }
+  return FDA_OK;
+}
+
 fda_status fda_plan_destroy(fda_plan P) {
   if (!P) return FDA_ERR_INVALID_ARG;
+  if (P->comm) fda::nccl().CommDestroy(P->comm);
+  if (P->ev_up) cudaEventDestroy(P->ev_up);
+  if (P->ev_x) cudaEventDestroy(P->ev_x);
+  if (P->xstream) cudaStreamDestroy(P->xstream);
   free_plan(P);
   delete P;
   return FDA_OK;

@@ -124,6 +124,44 @@ void launch_unpermute(int64_t n, const int32_t* perm, const double2* outm, doubl
   k_unpermute<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, outm, out);
 }
 
+// ---------------------------------------------------------------- multi-GPU expansion exchange
+// pack: warp per send entry, buf[boff[e] + k] = X[xoff[e] + k], k < len[e]
+__global__ void k_xpack(int64_t nent, const int64_t* __restrict__ xoff, const int32_t* __restrict__ len,
+                        const int64_t* __restrict__ boff, const double2* __restrict__ X, double2* __restrict__ buf) {
+  const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  if (e >= nent) return;
+  const int lane = threadIdx.x & 31;
+  const double2* src = X + xoff[e];
+  double2* dst = buf + boff[e];
+  for (int k = lane; k < len[e]; k += 32) dst[k] = src[k];
+}
+void launch_xpack(int64_t nent, const int64_t* xoff, const int32_t* len, const int64_t* boff, const double2* X,
+                  double2* buf, cudaStream_t st) {
+  if (nent <= 0) return;
+  k_xpack<<<(unsigned)((nent * 32 + 255) / 256), 256, 0, st>>>(nent, xoff, len, boff, X, buf);
+}
+// unpack: warp per destination slot, X[xoff[d] + k] += sum over its received partials (peer order), so the
+// sum is deterministic and needs no atomics
+__global__ void k_xunpack(int64_t ndst, const int64_t* __restrict__ xoff, const int32_t* __restrict__ len,
+                          const int64_t* __restrict__ rptr, const int64_t* __restrict__ roff,
+                          const double2* __restrict__ buf, double2* __restrict__ X) {
+  const int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  if (d >= ndst) return;
+  const int lane = threadIdx.x & 31;
+  double2* dst = X + xoff[d];
+  const int64_t pb = rptr[d], pe = rptr[d + 1];
+  for (int k = lane; k < len[d]; k += 32) {
+    double2 a = dst[k];
+    for (int64_t p = pb; p < pe; ++p) a = cadd(a, buf[roff[p] + k]);
+    dst[k] = a;
+  }
+}
+void launch_xunpack(int64_t ndst, const int64_t* xoff, const int32_t* len, const int64_t* rptr, const int64_t* roff,
+                    const double2* buf, double2* X, cudaStream_t st) {
+  if (ndst <= 0) return;
+  k_xunpack<<<(unsigned)((ndst * 32 + 255) / 256), 256, 0, st>>>(ndst, xoff, len, rptr, roff, buf, X);
+}
+
 // ---------------------------------------------------------------- H2 P2P near field
 #define P2P_T 128
 #define P2P_MAXL 256
@@ -443,8 +481,8 @@ __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ A
   if (ct >= 4 && GT_P / 8 >= 4)
     gt_stage<GT_P, MODE, (GT_P / 8 >= 4 ? 4 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt,
                                                       wbase, nw);
-  else if (ct >= 2)
-    gt_stage<GT_P, MODE, 2, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
+  else if (ct >= 2 && GT_P / 8 >= 2)
+    gt_stage<GT_P, MODE, (GT_P / 8 >= 2 ? 2 : 1), ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
   else
     gt_stage<GT_P, MODE, 1, ASM>(Ag, Mt, Kt, ksplit, Bs, ldb, Ts, ldt, Y, sOut, s_out, nb, lda_kt, wbase, nw);
 }
@@ -708,21 +746,41 @@ static size_t gt_smem(const GTrans& T, int p, int nbuf, bool stage) {
   return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2) +
          (stage ? (size_t)T.mmax * sizeof(double) : 0);
 }
+// opt-in shared-memory limit per CTA of the current device (227 KB on B200)
+static size_t smem_optin() {
+  static size_t v = 0;
+  if (!v) {
+    int dev = 0, b = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || b <= 0) {
+      cudaGetLastError();
+      b = 227 * 1024;
+    }
+    v = (size_t)b;
+  }
+  return v;
+}
 // chunk width, buffering and matrix staging: the first candidate that keeps two CTAs per SM
-// (FDA_GT_STAGE=0 disables staging)
+// (FDA_GT_STAGE=0 disables staging); else the widest single-buffered chunk that fits one CTA per SM
+// (large expansions at small eps: s_in ~ 1000 surface points); 8 columns as the last resort.
 static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
   static const bool allow = !(getenv("FDA_GT_STAGE") && getenv("FDA_GT_STAGE")[0] == '0');
   const int cand[6][3] = {{32, 1, 1}, {32, 2, 0}, {32, 1, 0}, {16, 1, 1}, {16, 2, 0}, {16, 1, 0}};
+  static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
+                                                         : (size_t)GT_SMEM_BUDGET;
   for (auto& c : cand) {
     if (c[2] && !allow) continue;
-    static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
-                                                           : (size_t)GT_SMEM_BUDGET;
     if (gt_smem(T, c[0], c[1], c[2]) <= budget) {
       *p = c[0], *nbuf = c[1], *stage = c[2];
       return;
     }
   }
-  *p = 16, *nbuf = 1, *stage = false;
+  for (int pp : {32, 16})
+    if (gt_smem(T, pp, 1, false) <= smem_optin()) {
+      *p = pp, *nbuf = 1, *stage = false;
+      return;
+    }
+  *p = 8, *nbuf = 1, *stage = false;
 }
 size_t gtrans_smem(const GTrans& T) {
   int p, nb;
@@ -730,6 +788,7 @@ size_t gtrans_smem(const GTrans& T) {
   gt_cfg(T, &p, &nb, &stg);
   return gt_smem(T, p, nb, stg);
 }
+bool gtrans_fits(const GTrans& T) { return T.n_items <= 0 || gtrans_smem(T) <= smem_optin(); }
 int gtrans_cols(const GTrans& T) {
   int p, nb;
   bool stg;
@@ -738,9 +797,11 @@ int gtrans_cols(const GTrans& T) {
 }
 
 template <int P, int NB, bool STG>
-static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(k_gtrans<P, NB, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+static cudaError_t gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_gtrans<P, NB, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
   // One CTA per item (the hardware block scheduler keeps the resident items a compact window of the
   // Morton launch order).  FDA_GT_PERSIST=1: persistent CTAs streaming items b, b+G, ... -- measured
   // slower at config 5 (348 vs 336 ms: the CTAs drift apart in the item order and the L2 window grows).
@@ -754,6 +815,7 @@ static void gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, 
     grid = std::min<int64_t>(T.n_items, (int64_t)std::max(1, per_sm) * nsm);
   }
   k_gtrans<P, NB, STG><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
+  return cudaGetLastError();
 }
 
 // largest pad8 rank for which the warp-specialised kernel (32 columns, X + 2 T tiles) fits the budget
@@ -766,13 +828,17 @@ int gtrans_ws_rmax(int s_in) {
 }
 
 template <bool STG>
-static void gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_gtrans_ws<32, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+static cudaError_t gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_gtrans_ws<32, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
   k_gtrans_ws<32, STG><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  return cudaGetLastError();
 }
 
-void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
-  if (T.n_items <= 0) return;
+cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
+  if (T.n_items <= 0) return cudaSuccess;
   // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
   static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
   if (ws_ok && T.atomic && T.all_lowrank) {
@@ -785,12 +851,13 @@ void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t s
   bool stg;
   gt_cfg(T, &p, &nb, &stg);
   const size_t sm = gt_smem(T, p, nb, stg);
-  if (p == 32 && nb == 1 && stg) gt_launch<32, 1, true>(T, X, Y, sm, st);
-  else if (p == 32 && nb == 2) gt_launch<32, 2, false>(T, X, Y, sm, st);
-  else if (p == 32) gt_launch<32, 1, false>(T, X, Y, sm, st);
-  else if (stg) gt_launch<16, 1, true>(T, X, Y, sm, st);
-  else if (nb == 2) gt_launch<16, 2, false>(T, X, Y, sm, st);
-  else gt_launch<16, 1, false>(T, X, Y, sm, st);
+  if (p == 32 && nb == 1 && stg) return gt_launch<32, 1, true>(T, X, Y, sm, st);
+  if (p == 32 && nb == 2) return gt_launch<32, 2, false>(T, X, Y, sm, st);
+  if (p == 32) return gt_launch<32, 1, false>(T, X, Y, sm, st);
+  if (p == 16 && stg) return gt_launch<16, 1, true>(T, X, Y, sm, st);
+  if (p == 16 && nb == 2) return gt_launch<16, 2, false>(T, X, Y, sm, st);
+  if (p == 16) return gt_launch<16, 1, false>(T, X, Y, sm, st);
+  return gt_launch<8, 1, false>(T, X, Y, sm, st);
 }
 
 // ---------------------------------------------------------------- H8 L2T

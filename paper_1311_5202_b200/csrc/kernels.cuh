@@ -24,6 +24,12 @@ struct Points {
 void launch_permute_scale(int64_t n, const int32_t* perm, const double* w, const double2* phi, double2* q,
                           double2* phim, cudaStream_t st);
 void launch_unpermute(int64_t n, const int32_t* perm, const double2* outm, double2* out, cudaStream_t st);
+// multi-GPU expansion exchange: gather send entries of the concatenated outgoing expansions X into buf;
+// add each destination slot's received partial sums (CSR rptr/roff into buf, peer order) into X
+void launch_xpack(int64_t nent, const int64_t* xoff, const int32_t* len, const int64_t* boff, const double2* X,
+                  double2* buf, cudaStream_t st);
+void launch_xunpack(int64_t ndst, const int64_t* xoff, const int32_t* len, const int64_t* rptr, const int64_t* roff,
+                    const double2* buf, double2* X, cudaStream_t st);
 // kind 0: BM_H kernel (dG/dn_y + alpha d2G/dn_x dn_y), 1: BM_G kernel (G + alpha dG/dn_x),
 // 2: Table-1 kernel (G + alpha dG/dn_y)
 void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
@@ -62,8 +68,9 @@ struct GTrans {
   int ct1 = 0, ct2 = 0;                 // warp-unit column tiles (experiments: FDA_GT_CT1 / FDA_GT_CT2; 0 = default, -1 = balance)
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
 };
-void launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
+cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
+bool gtrans_fits(const GTrans& T);    // gtrans_smem(T) within the device's opt-in shared-memory limit
 int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)
 int gtrans_ws_rmax(int s_in);         // largest (pad8) low rank the warp-specialised kernel takes
 

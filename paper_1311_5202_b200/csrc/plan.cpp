@@ -492,7 +492,9 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     // one more surface point per edge for each decade of eps below 1e-4 (measured: the LF surface
     // resolution caps the accuracy below 1e-4, profiles/r01_eps_probe.jsonl; unchanged at eps >= 1e-4)
     const int dp = eps < 1e-4 ? (int)std::lround(std::log10(1e-4 / eps)) : 0;
-    L.p = (wl < opt.lf_p_switch ? opt.lf_p_low : opt.lf_p_high) + dp;
+    // explicit lf_p_low / lf_p_high options are used verbatim; the eps bump applies to the defaults only
+    const int p_low = opt.lf_p_low > 0 ? opt.lf_p_low : 6 + dp, p_high = opt.lf_p_high > 0 ? opt.lf_p_high : 8 + dp;
+    L.p = wl < opt.lf_p_switch ? p_low : p_high;
     L.eq_pts = surface_grid(L.p, 1.05 * L.w);  // outgoing equivalent = incoming check (inner)
     L.ck_pts = surface_grid(L.p, 2.95 * L.w);  // outgoing check = incoming equivalent (outer)
     L.nsurf = (int)L.eq_pts.size();

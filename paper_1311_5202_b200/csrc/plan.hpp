@@ -24,8 +24,8 @@ struct Options {
   int np = 0;               // leaf threshold N_p; 0 -> from eps (eq_npleaf, sign-corrected)
   double eps_int = 0;       // expansion truncation tolerance; 0 -> eps / 100 (R11)
   double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps / 3 (R23)
-  int lf_p_low = 6;         // LF surface points per edge for w/lambda < lf_p_switch
-  int lf_p_high = 8;        // ... for w/lambda >= lf_p_switch
+  int lf_p_low = 0;         // LF surface points per edge for w/lambda < lf_p_switch; 0 -> 6 + dp(eps)
+  int lf_p_high = 0;        // ... for w/lambda >= lf_p_switch; 0 -> 8 + dp(eps)  (R17)
   double lf_p_switch = 0.75;
   int lowrank = 1;          // low-rank M2L (eq_lrdk) on/off
   int single_leaf = 0;      // debug: no far field, root is the only leaf (everything P2P)
@@ -84,6 +84,8 @@ struct Level {
   std::vector<int> dir_rep;      // dir -> index into reps
   std::vector<Sym> dir_sym;      // dir -> g with P_dir = g P_rep
   std::vector<DirRep> reps;
+  // the expansion length of direction d (HF wedges are truncated separately; s is their maximum)
+  int sdir(int d) const { return hf && !reps.empty() ? (int)reps[dir_rep[d]].sig.size() : s; }
 };
 
 struct HostPlan {

@@ -24,13 +24,15 @@ STATUS = {0: "FDA_OK", 1: "FDA_ERR_INVALID_ARG", 2: "FDA_ERR_COINCIDENT_POINTS",
           4: "FDA_ERR_CUDA", 5: "FDA_ERR_OOM", 6: "FDA_ERR_SETUP_ACCURACY", 7: "FDA_ERR_NCCL", 8: "FDA_ERR_STATE"}
 FDA_PHASE_NEAR, FDA_PHASE_CORR, FDA_PHASE_FAR, FDA_PHASE_ALL = 1, 2, 4, 7
 FDA_KERNEL_BMH, FDA_KERNEL_BMG, FDA_KERNEL_T1 = 0, 1, 2
-PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute")
+PHASES = ("permute", "p2p", "csr", "s2m", "m2m", "m2l", "l2l", "l2t", "unpermute", "exchange")
+FDA_NPHASES = len(PHASES)
 
 # every symbol include/fda.h declares (checked by tests/test_abi.py)
 EXPORTS = ("fda_options_default", "fda_plan_create", "fda_plan_create_ex", "fda_plan_set_correction", "fda_apply",
            "fda_apply_phases", "fda_apply_timed", "fda_plan_set_stream", "fda_plan_stats", "fda_plan_log",
            "fda_plan_export_leaves", "fda_plan_export_p2p", "fda_plan_export_m2l", "fda_plan_destroy",
-           "fda_status_str", "fda_plan_launches")
+           "fda_status_str", "fda_plan_launches", "fda_nccl_unique_id", "fda_plan_create_dist", "fda_dist_counts",
+           "fda_apply_up", "fda_apply_down", "fda_plan_export_exchange")
 
 
 class fda_options(ctypes.Structure):
@@ -48,7 +50,8 @@ class fda_stats(ctypes.Structure):
                  "owned_end", "owned_leaf_begin", "owned_leaf_end")] + \
                [(f, ctypes.c_double) for f in
                 ("setup_tree_s", "setup_lists_s", "setup_ops_s", "setup_upload_s", "flops_p2p", "flops_m2l",
-                 "flops_m2m", "flops_l2l", "flops_s2m", "flops_l2t", "bytes_csr")]
+                 "flops_m2m", "flops_l2l", "flops_s2m", "flops_l2t", "bytes_csr")] + \
+               [(f, ctypes.c_int64) for f in ("s2m_evals", "l2t_evals", "xchg_send_bytes", "xchg_recv_bytes")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -77,6 +80,13 @@ _lib.fda_status_str.argtypes = [ctypes.c_int]
 _lib.fda_status_str.restype = ctypes.c_char_p
 _lib.fda_plan_launches.argtypes = [_P]
 _lib.fda_plan_launches.restype = ctypes.c_int64
+_lib.fda_nccl_unique_id.argtypes = [ctypes.c_char_p]
+_lib.fda_plan_create_dist.argtypes = [_I64, _P, _P, _P, _D, _D, _D, _D, ctypes.POINTER(fda_options), ctypes.c_char_p,
+                                      ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
+_lib.fda_dist_counts.argtypes = [_P, _P, _P]
+_lib.fda_apply_up.argtypes = [_P, _P, _P]
+_lib.fda_apply_down.argtypes = [_P, _P, _P]
+_lib.fda_plan_export_exchange.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), _P, _P, _P]
 
 
 class FDAError(RuntimeError):
@@ -142,7 +152,7 @@ def fda_apply_phases(plan, mask, phi, out):
 
 
 def fda_apply_timed(plan, mask, phi, out):
-    ms = (ctypes.c_float * 9)()
+    ms = (ctypes.c_float * FDA_NPHASES)()
     _check(_lib.fda_apply_timed(plan, int(mask), _ptr(phi), _ptr(out), ms), "fda_apply_timed")
     return dict(zip(PHASES, list(ms)))
 
@@ -189,6 +199,57 @@ def fda_plan_export_m2l(plan):
     s = np.empty((npairs.value, 3), np.int64)
     _check(_lib.fda_plan_export_m2l(plan, ctypes.byref(npairs), _ptr(lev), _ptr(t), _ptr(s)), "fda_plan_export_m2l")
     return lev, t, s
+
+
+def fda_nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 makes it; the caller distributes it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fda_nccl_unique_id(buf), "fda_nccl_unique_id")
+    return buf.raw
+
+
+def fda_plan_create_dist(points, normals, quad_weights, k, alpha, eps, nccl_id: bytes, rank: int, nranks: int,
+                         options: fda_options | None = None):
+    """Collective plan over nranks processes (one GPU each); fda_apply then returns the full out on every rank."""
+    if len(nccl_id) != 128:
+        raise ValueError("nccl_id must be the 128 bytes of fda_nccl_unique_id()")
+    n = int(points.shape[0])
+    h = _P()
+    a = complex(alpha)
+    opt = options if options is not None else fda_options_default()
+    _check(_lib.fda_plan_create_dist(n, _ptr(points), _ptr(normals), _ptr(quad_weights), float(k), a.real, a.imag,
+                                     float(eps), ctypes.byref(opt), ctypes.create_string_buffer(nccl_id, 128),
+                                     int(rank), int(nranks), ctypes.byref(h)), "fda_plan_create_dist")
+    return h
+
+
+def fda_dist_counts(plan, nranks: int):
+    """(send_counts, recv_counts) per peer, complex128 elements."""
+    s = np.zeros(nranks, np.int64)
+    r = np.zeros(nranks, np.int64)
+    _check(_lib.fda_dist_counts(plan, _ptr(s), _ptr(r)), "fda_dist_counts")
+    return s, r
+
+
+def fda_apply_up(plan, phi, sendbuf):
+    _check(_lib.fda_apply_up(plan, _ptr(phi), _ptr(sendbuf)), "fda_apply_up")
+
+
+def fda_apply_down(plan, recvbuf, out):
+    _check(_lib.fda_apply_down(plan, _ptr(recvbuf), _ptr(out)), "fda_apply_down")
+
+
+def fda_plan_export_exchange(plan, peer: int, recv: bool):
+    """(level, slot, cube_ijk) of the entries this rank sends to (recv=False) / receives from (True) peer."""
+    cnt = _I64()
+    _check(_lib.fda_plan_export_exchange(plan, int(peer), int(recv), ctypes.byref(cnt), None, None, None),
+           "fda_plan_export_exchange")
+    lev = np.empty(cnt.value, np.int32)
+    slot = np.empty(cnt.value, np.int64)
+    ijk = np.empty((cnt.value, 3), np.int64)
+    _check(_lib.fda_plan_export_exchange(plan, int(peer), int(recv), ctypes.byref(cnt), _ptr(lev), _ptr(slot),
+                                         _ptr(ijk)), "fda_plan_export_exchange")
+    return lev, slot, ijk
 
 
 def fda_plan_destroy(plan):

@@ -320,6 +320,14 @@ def random_phi(n: int, seed: int) -> np.ndarray:
     return np.ascontiguousarray(v[:, 0] + 1j * v[:, 1])
 
 
+def plane_wave(x: np.ndarray, k: float, d=(0.0, 0.6, 0.8)) -> np.ndarray:
+    """Smooth density phi_j = e^{ik d.x_j}, |d| = 1: the incident plane wave of PAPER.md:1043-1048, used as a
+    density whose far field does not cancel (the random density's far field largely does)."""
+    d = np.asarray(d, dtype=np.float64)
+    d = d / np.linalg.norm(d)
+    return np.ascontiguousarray(np.exp(1j * float(k) * (np.asarray(x) @ d)))
+
+
 def sample_rows(n: int, count: int, seed: int) -> np.ndarray:
     """Seeded target-row sample (SURVEY.md §8(c) #10)."""
     if count >= n:

@@ -160,37 +160,3 @@ def test_full_apply_full_oracle(name, nu, k, opts):
     far_err = oracle.rel_l2(got - near, ref - near)
     print(f"{name}: N={p.N} rel l2 {err:.3e}  far-only {far_err:.3e}")
     assert err <= 1e-4
-
-
-@pytest.mark.parametrize("nranks", [2, 3])
-def test_rank_partitioned_applies_sum_to_single(nranks):
-    """The multi-GPU decomposition on one device: the applies of the rank plans
-    (rank r of R owns a Morton range of leaves; other rows are zero) sum to the single-rank apply.
-    Run sequentially on one GPU (no rank waits on another)."""
-    fda = _fda()
-    p = synth.make_problem("x", k=50.0, nu=16)            # HF + LF levels
-    csr = p.correction(seed=3)
-    phi = synth.random_phi(p.N, 5)
-    h = _plan(p)
-    try:
-        fda.fda_plan_set_correction(h, csr[0], csr[1], csr[2].view(np.float64))
-        full = _run(h, phi)
-    finally:
-        fda.fda_plan_destroy(h)
-    acc = np.zeros_like(full)
-    owned = np.zeros(p.N, dtype=np.int64)
-    for r in range(nranks):
-        hr = _plan(p, rank=r, nranks=nranks)
-        try:
-            fda.fda_plan_set_correction(hr, csr[0], csr[1], csr[2].view(np.float64))
-            part = _run(hr, phi)
-            lop, lev, ijk = fda.fda_plan_export_leaves(hr, p.N)
-            st = fda.fda_plan_stats(hr)
-        finally:
-            fda.fda_plan_destroy(hr)
-        mine = (lop >= st["owned_leaf_begin"]) & (lop < st["owned_leaf_end"])
-        assert np.all(part[~mine] == 0)                    # rows outside the owned range stay zero
-        owned += mine
-        acc += part
-    assert np.all(owned == 1)
-    assert oracle.rel_l2(acc, full) <= 1e-13              # same arithmetic up to atomic summation order

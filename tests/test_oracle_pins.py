@@ -295,3 +295,63 @@ def test_p3_table1_kernel_reciprocity():
         assert abs(t1 - oracle.kernel(oracle.KIND_BMG, y, b, x, a, k, al)) <= 1e-14 * abs(t1)
         parts = oracle.kernel(oracle.KIND_G, x, None, y, None, k) + al * oracle.kernel(oracle.KIND_DNY, x, None, y, b, k)
         assert abs(t1 - parts) <= 1e-14 * abs(t1)
+
+
+# --------------------------------------------------------------- oracle_near: the leaf-pair restriction
+def _near_brute(K, phi, members, pairs):
+    """Brute force of the restricted sum from a dense kernel matrix built by single oracle.kernel calls:
+    out_i = sum over listed leaf pairs (t, s) with i in t, j in s, j != i of K_ij phi_j."""
+    out = np.zeros(K.shape[0], dtype=np.complex128)
+    for t, s in pairs:
+        for i in members[t]:
+            for j in members[s]:
+                if j != i:
+                    out[i] += K[i, j] * phi[j]
+    return out
+
+
+@pytest.mark.parametrize("kind", [oracle.KIND_BMH, oracle.KIND_BMG])
+def test_oracle_near_multi_leaf_pairs(kind):
+    """oracle_near (the <= 1e-12 reference of the P2P parity) on >= 8 'leaves' of a random
+    cloud, given as shuffled, non-contiguous point-index lists of unequal sizes:
+      * all leaf pairs including self pairs  ==  oracle_rows (the whole j != i sum);
+      * a random subset of pairs             ==  brute force from a dense single-call kernel matrix;
+      * two disjoint halves of the pair list add up to the whole list.
+    A wrong index in the pair loop (source range taken from the target leaf, a skipped self pair, the
+    j != i test on leaf-local instead of global indices) fails one of these."""
+    p = synth.make_problem("x", k=4.0, nu=3)      # N = 432 surface points
+    N = p.N
+    rng = np.random.default_rng(21)
+    phi = synth.random_phi(N, 8)
+    nleaf = 11
+    perm = rng.permutation(N)
+    cuts = np.sort(rng.choice(np.arange(1, N), nleaf - 1, replace=False))
+    members = np.split(perm, cuts)
+    leaf_ptr = np.concatenate([[0], np.cumsum([len(m) for m in members])])
+    leaf_pts = np.concatenate(members)
+    all_pairs = [(t, s) for t in range(nleaf) for s in range(nleaf)]
+
+    def near(pairs):
+        pairs = sorted(pairs)
+        tgt = np.array([t for t, _ in pairs], dtype=np.int64)
+        src = np.array([s for _, s in pairs], dtype=np.int64)
+        pair_ptr = np.concatenate([[0], np.cumsum(np.bincount(tgt, minlength=nleaf))])
+        return oracle.apply_near(p.x, p.n, p.w, p.k, p.alpha, phi, leaf_ptr, leaf_pts, pair_ptr, src, kind=kind)
+
+    full = oracle.apply_rows(p.x, p.n, p.w, p.k, p.alpha, phi, kind=kind)
+    got = near(all_pairs)
+    assert np.abs(got - full).max() <= 1e-13 * np.abs(full).max()
+    K = np.array([[0 if i == j else p.w[j] * oracle.kernel(kind, p.x[i], p.n[i], p.x[j], p.n[j], p.k, p.alpha)
+                   for j in range(N)] for i in range(N)])
+    sel = [all_pairs[i] for i in rng.choice(len(all_pairs), 40, replace=False)]
+    a = near(sel)
+    b = _near_brute(K, phi, members, sel)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+    # rows of targets in no listed pair are exactly zero
+    listed = np.zeros(N, bool)
+    for t, _ in sel:
+        listed[members[t]] = True
+    assert np.all(a[~listed] == 0)
+    half = set(sel[:20])
+    rest = [q for q in all_pairs if q not in half]
+    assert np.abs(near(list(half)) + near(rest) - full).max() <= 1e-13 * np.abs(full).max()

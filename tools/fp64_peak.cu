@@ -5,8 +5,10 @@
 // (1) DFMA: every thread runs 8 independent FMA chains; 148 SMs x many warps.
 // (2) DMMA: warp-level mma.sync.aligned.m8n8k4.row.col.f64 (the FP64 tensor path of sm_80+).
 // (3) sincos + rsqrt throughput (the P2P kernel's transcendental mix), in evaluations/s.
-// Prints one JSON line: {"dfma_tflops":..., "dmma_tflops":..., "sincos_geval_s":..., "sm_mhz": ...}
+// Prints one JSON line per repetition (argv[1] repetitions, default 1; tools/fp64_peak.py samples the
+// SM clock with nvidia-smi meanwhile): {"dfma_tflops":..., "dmma_tflops":..., "sincos_geval_s":..., "sm_mhz": ...}
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void k_dfma(double* out, int iters, double a, double b) {
@@ -53,7 +55,7 @@ __global__ void k_sincos(double* out, int iters, double k) {
   if (acc == 12345.678) out[0] = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
   double* d;
   cudaMalloc(&d, 8);
   cudaEvent_t e0, e1;
@@ -64,6 +66,8 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const int blocks = sms * 8, threads = 256;
   float ms;
+  const int reps = argc > 1 ? atoi(argv[1]) : 1;
+  for (int rep = 0; rep < reps; ++rep) {
   // DFMA
   const int it1 = 20000;
   k_dfma<<<blocks, threads>>>(d, 100, 1.0000001, 1e-9);
@@ -95,5 +99,7 @@ int main() {
   printf("{\"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"sincos_rsqrt_geval_s\": %.3f, \"sms\": %d, "
          "\"clock_rate_mhz_attr\": %d, \"err\": \"%s\"}\n",
          dfma, dmma, sc, sms, clk / 1000, cudaGetErrorString(err));
+  fflush(stdout);
+  }
   return 0;
 }

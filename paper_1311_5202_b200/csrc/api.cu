@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "nccl_dl.hpp"
 #include "plan.hpp"
+#include "plan_dev.cuh"
 
 using fda::cplx;
 
@@ -84,7 +85,8 @@ struct fda_plan_s {
     double2 *sendbuf = nullptr, *recvbuf = nullptr;
   } xc;
   double2* Xall = nullptr;
-  std::vector<int64_t> xoff;  // per level offset (complex128 elements) into Xall
+  std::vector<int64_t> xoff;
+  std::vector<fda::DevSet> dev_sets;  // point sets / factors of the device-built operators  // per level offset (complex128 elements) into Xall
   ncclComm_t comm = nullptr;  // fda_plan_create_dist
   cudaStream_t xstream = nullptr;
   cudaEvent_t ev_up = nullptr, ev_x = nullptr;
@@ -223,17 +225,35 @@ std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s
   return pool;
 }
 
+// Fragment-order size (doubles) of a group's operator: dense s_out x s_in, or V (r x s_in) then U (s_out x r).
+int64_t frag_size(int rank, int s_out, int s_in) {
+  if (rank < 0) return (int64_t)(pad8(s_out) / 8) * (pad4(s_in) / 4) * 64;
+  return (int64_t)(pad8(rank) / 8) * (pad4(s_in) / 4) * 64 + (int64_t)(pad8(s_out) / 8) * (pad8(rank) / 8) * 64;
+}
+
+// Work items of a grouped translation.  raw != nullptr: the groups' matrices are the host column-major pool
+// raw (G.mat offsets), converted to fragment order and uploaded; raw == nullptr: they are already in the
+// device pool dpool in fragment order (G.mat = offsets in doubles, plan_dev.cu).
 fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& out_cube,
-                       const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, const cplx* raw) {
+                       const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, const cplx* raw,
+                       const double* dpool = nullptr) {
   fda::GTrans T;
   const int64_t ng = (int64_t)G.rank.size(), np = (int64_t)G.out.size();
   if (np == 0) return T;
   {
     int rmax8 = 0;
     int64_t mmax = 0;
-    std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8, &mmax);
+    if (raw) {
+      std::vector<double> pool = frag_pool(G, raw, s_out, s_in, &rmax8, &mmax);
+      T.pool = upload(P, pool);
+    } else {
+      for (int32_t r : G.rank) {
+        if (r >= 0) rmax8 = std::max(rmax8, pad8(r));
+        mmax = std::max<int64_t>(mmax, frag_size(r, s_out, s_in));
+      }
+      T.pool = dpool;
+    }
     T.mmax = mmax;
-    T.pool = upload(P, pool);
     T.rmax8 = rmax8;
     T.s_out = s_out, T.s_in = s_in;
     T.all_lowrank = 1;
@@ -381,7 +401,9 @@ void set_ownership(fda_plan P, const fda_options& o) {
     std::vector<double> cf(H.cubes.size(), 0.0);
     for (const auto& g : H.m2l_groups) {
       const fda::Level& L = H.levels[g.level];
-      const double f = g.rank < 0 ? 8.0 * L.s * L.s : 16.0 * g.rank * L.s;
+      // device-built operators have no rank yet (-2): estimate r = s / 6 (config 5 measures 13-15 at s = 58-136)
+      const double r = g.rank == -2 ? L.s / 6.0 : g.rank;
+      const double f = g.rank == -1 ? 8.0 * L.s * L.s : 16.0 * r * L.s;
       for (int64_t p = g.pbeg; p < g.pend; ++p) cf[L.cubes[L.in_cube[H.m2l_tgt[p]]]] += f;
     }
     for (int64_t t = 0; t < nl; ++t) {
@@ -530,11 +552,62 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     if (L.n_out) D.X = P->Xall + P->xoff[l];
     if (L.n_in) D.Y = dalloc<double2>(P, (size_t)L.n_in * L.s);
   }
-  // M2L: pairs filtered to owned targets, grouped by offset, split into owned work items
+  // device point sets and factors of every level's directions (plan_dev.cuh DevSet), for the operators
+  const bool dev_ops = H.opt.dev_ops;
+  std::vector<std::vector<int>> bset(nlev), aset(nlev);
+  fda::DevSet* d_sets = nullptr;
+  if (dev_ops) {
+    std::vector<fda::DevSet> hs;
+    auto up_c = [&](const std::vector<cplx>& v) { return reinterpret_cast<const double2*>(upload(P, v)); };
+    for (int l = std::max(H.lmin, 0); H.lmin >= 0 && l < nlev; ++l) {
+      const fda::Level& L = H.levels[l];
+      if (L.s == 0 || (L.n_out == 0 && L.n_in == 0)) continue;
+      const int nd = L.hf ? L.ndir : 1;
+      bset[l].assign(nd, -1), aset[l].assign(nd, -1);
+      // factors per representative (HF) or of the LF surface: V, V^T (M2L left), Sigma^-1 U^H (M2M left)
+      const int nrep = L.hf ? (int)L.reps.size() : 1;
+      std::vector<const double2*> fV(nrep), fVT(nrep), fSU(nrep);
+      std::vector<int> fs(nrep);
+      for (int ri = 0; ri < nrep; ++ri) {
+        const fda::Mat& U = L.hf ? L.reps[ri].U : L.lfU;
+        const fda::Mat& V = L.hf ? L.reps[ri].V : L.lfV;
+        const std::vector<double>& sg = L.hf ? L.reps[ri].sig : L.lfsig;
+        const int sr = (int)sg.size();
+        std::vector<cplx> vt((size_t)sr * V.m), su((size_t)sr * U.m);
+        for (int64_t i = 0; i < V.m; ++i)
+          for (int r = 0; r < sr; ++r) vt[r + (size_t)i * sr] = V(i, r);
+        for (int64_t i = 0; i < U.m; ++i)
+          for (int r = 0; r < sr; ++r) su[r + (size_t)i * sr] = std::conj(U(i, r)) / sg[r];
+        fV[ri] = up_c(V.a), fVT[ri] = up_c(vt), fSU[ri] = up_c(su), fs[ri] = sr;
+      }
+      for (int d = 0; d < nd; ++d) {
+        if (L.hf && L.dir_rep[d] < 0) continue;
+        const int ri = L.hf ? L.dir_rep[d] : 0;
+        auto pts = [&](bool check) {
+          std::vector<double> f;
+          for (const auto& p : fda::dir_points(L, d, check)) f.insert(f.end(), {p[0], p[1], p[2]});
+          return f;
+        };
+        const std::vector<double> pb = pts(false), pa = pts(true);
+        bset[l][d] = (int)hs.size();
+        hs.push_back(fda::DevSet{(int)pb.size() / 3, fs[ri], upload(P, pb), fVT[ri], fV[ri]});
+        aset[l][d] = (int)hs.size();
+        hs.push_back(fda::DevSet{(int)pa.size() / 3, fs[ri], upload(P, pa), fSU[ri], nullptr});
+      }
+    }
+    d_sets = upload(P, hs);
+    P->dev_sets = hs;
+  }
+  auto set_max = [&](const std::vector<int>& ids, int* maxn) {
+    for (int i : ids) *maxn = std::max(*maxn, P->dev_sets[i].n);
+  };
+  // M2L: pairs filtered to owned targets, grouped by offset; operators built on the device
   for (int l = 0; l < nlev; ++l) {
     const fda::Level& L = H.levels[l];
     GroupedPairs G;
-    for (const auto& g : H.m2l_groups) {
+    std::vector<int64_t> gid;  // group index in H.m2l_groups
+    for (size_t gi = 0; gi < H.m2l_groups.size(); ++gi) {
+      const auto& g = H.m2l_groups[gi];
       if (g.level != l) continue;
       const size_t b0 = G.out.size();
       for (int64_t p = g.pbeg; p < g.pend; ++p) {
@@ -547,15 +620,61 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       G.gptr.push_back((int64_t)G.out.size());
       G.rank.push_back(g.rank);
       G.mat.push_back(g.mat_off);
-      const double np = (double)(G.out.size() - b0);
-      P->st.m2l_pairs += (int64_t)np;
-      P->st.m2l_groups += 1;
-      P->st.m2l_lowrank_groups += g.rank >= 0;
-      // algorithmic flops with the wedges' own expansion lengths (the pool pads them to the level's max)
-      const double ss = L.sdir(g.dir), st_ = L.sdir(L.hf ? fda::anti_dir(g.dir, L.m) : 0);
-      P->st.flops_m2l += np * (g.rank < 0 ? 8.0 * st_ * ss : 8.0 * g.rank * (st_ + ss));
+      gid.push_back((int64_t)gi);
     }
     if (G.out.empty()) continue;
+    const double* dpool = nullptr;
+    if (dev_ops) {
+      // K~ of every group on the device: pass 1 ranks, offsets, pass 2 the fragment-order pool
+      const int ng = (int)gid.size();
+      std::vector<int32_t> ia(ng), ib(ng);
+      std::vector<double> sh(3 * (size_t)ng);
+      std::vector<int> used_sets;
+      for (int g = 0; g < ng; ++g) {
+        const auto& hg = H.m2l_groups[gid[g]];
+        const int d = L.hf ? hg.dir : 0, t = L.hf ? fda::anti_dir(hg.dir, L.m) : 0;
+        ia[g] = bset[l][t], ib[g] = bset[l][d];
+        for (int c = 0; c < 3; ++c) sh[3 * g + c] = hg.off[c] * L.w;  // G(delta w + b_t - b_s)
+      }
+      fda::OpJob J;
+      J.n_items = ng;
+      J.a = upload(P, ia), J.b = upload(P, ib), J.shift = upload(P, sh);
+      J.sets = d_sets, J.k = H.k, J.s_out = L.s, J.s_in = L.s;
+      J.compress = H.opt.lowrank ? 1 : 0, J.eps_lr = H.eps_lr;
+      set_max(bset[l], &J.maxn);
+      J.maxs = L.s;
+      std::vector<int32_t> rk(ng, -1);
+      if (J.compress) {
+        int32_t* d_rank = dalloc<int32_t>(P, ng);
+        J.rank = d_rank;
+        ck(fda::launch_opjob(J, 1, 0));
+        ck(cudaMemcpy(rk.data(), d_rank, ng * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        J.rank_in = d_rank;
+      }
+      std::vector<int64_t> off(ng);
+      int64_t tot = 0;
+      for (int g = 0; g < ng; ++g) {
+        off[g] = tot;
+        tot += frag_size(rk[g], L.s, L.s);
+        G.rank[g] = rk[g], G.mat[g] = off[g];
+        P->H.m2l_groups[gid[g]].rank = rk[g];
+      }
+      double* pool = dalloc<double>(P, (size_t)tot);
+      J.off = upload(P, off), J.pool = pool;
+      ck(fda::launch_opjob(J, 2, 0));
+      dpool = pool;
+    }
+    for (size_t g = 0; g < G.rank.size(); ++g) {
+      const auto& hg = H.m2l_groups[gid[g]];
+      const double np = (double)(G.gptr[g + 1] - G.gptr[g]);
+      P->st.m2l_pairs += (int64_t)np;
+      P->st.m2l_groups += 1;
+      P->st.m2l_lowrank_groups += G.rank[g] >= 0;
+      // algorithmic flops with the wedges' own expansion lengths (the pool pads them to the level's max)
+      const double ss = L.sdir(hg.dir), st_ = L.sdir(L.hf ? fda::anti_dir(hg.dir, L.m) : 0);
+      P->st.flops_m2l += np * (G.rank[g] < 0 ? 8.0 * st_ * ss : 8.0 * G.rank[g] * (st_ + ss));
+    }
+    const cplx* raw = dev_ops ? nullptr : H.m2l_pool[l].data();
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
     // the nearest offsets) go to a second launch of the general kernel.
     const int rlim = fda::gtrans_ws_rmax(L.s);
@@ -568,10 +687,10 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       D.mat.push_back(G.mat[g]);
     }
     if (!G1.out.empty() && !G2.out.empty()) {
-      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
-      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
+      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
     } else {
-      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, H.m2l_pool[l].data());
+      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
     }
   }
   // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
@@ -581,7 +700,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const fda::Level& Lp = H.levels[T.lp];
     const fda::Level& Lc = H.levels[T.lp + 1];
     D.lp = T.lp, D.sp = T.sp, D.sc = T.sc;
-    const int64_t nmat = (int64_t)(T.pool.size() / std::max<size_t>(1, (size_t)T.sp * T.sc));
+    const int64_t nmat = (int64_t)T.need.size();
     // CSR by output slot -> group-major pairs, keeping the pairs keep(out slot, in slot) accepts
     auto grouped = [&](const std::vector<int64_t>& ptr, const std::vector<int64_t>& other,
                        const std::vector<int64_t>& mat, auto keep) {
@@ -621,13 +740,48 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       fdn += 8.0 * Lp.sdir(Lp.in_dir[ps]) * Lc.sdir(Lc.in_dir[cs]);
       return true;
     };
+    // M2M (and its transpose, L2L) operators on the device: one per (parent direction, child octant)
+    const double *dup = nullptr, *ddn = nullptr;
+    if (dev_ops && nmat > 0) {
+      std::vector<int32_t> ia(nmat), ib(nmat);
+      std::vector<double> sh(3 * (size_t)nmat);
+      for (int64_t t = 0; t < nmat; ++t) {
+        const int d = T.need[t].first, oc = T.need[t].second;
+        ia[t] = aset[T.lp][Lp.hf ? d : 0];
+        ib[t] = bset[T.lp + 1][Lc.hf ? fda::child_dir(d, Lp.m) : 0];
+        const double o[3] = {(((oc >> 2) & 1) ? 0.5 : -0.5) * Lc.w, (((oc >> 1) & 1) ? 0.5 : -0.5) * Lc.w,
+                             ((oc & 1) ? 0.5 : -0.5) * Lc.w};
+        for (int c = 0; c < 3; ++c) sh[3 * t + c] = -o[c];  // E_up = G(a_P - (b_C + o))
+      }
+      fda::OpJob J;
+      J.n_items = (int)nmat;
+      J.a = upload(P, ia), J.b = upload(P, ib), J.shift = upload(P, sh);
+      J.sets = d_sets, J.k = H.k, J.s_out = T.sp, J.s_in = T.sc;
+      set_max(aset[T.lp], &J.maxn);
+      set_max(bset[T.lp + 1], &J.maxn);
+      J.maxs = std::max(T.sp, T.sc);
+      const int64_t szu = frag_size(-1, T.sp, T.sc), szd = frag_size(-1, T.sc, T.sp);
+      std::vector<int64_t> off(nmat);
+      for (int64_t t = 0; t < nmat; ++t) off[t] = t * szu;
+      double* pu = dalloc<double>(P, (size_t)(nmat * szu));
+      double* pd = dalloc<double>(P, (size_t)(nmat * szd));
+      J.off = upload(P, off), J.pool = pu, J.poolT = pd;
+      ck(fda::launch_opjob(J, 2, 0));
+      dup = pu, ddn = pd;
+    }
     if (!T.up_child.empty()) {
       GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat, up_keep);
-      D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc, T.pool.data());
+      if (dev_ops)
+        for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sp, T.sc);
+      D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc,
+                        dev_ops ? nullptr : T.pool.data(), dup);
     }
     if (!T.dn_parent.empty()) {
       GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat, dn_keep);
-      D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp, T.poolT.data());
+      if (dev_ops)
+        for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sc, T.sp);
+      D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp,
+                        dev_ops ? nullptr : T.poolT.data(), ddn);
     }
     P->st.flops_m2m += 0.5 * fup;  // keep() runs twice per pair (count, fill)
     P->st.flops_l2l += 0.5 * fdn;
@@ -751,6 +905,37 @@ void upload_exchange(fda_plan P) {
   X.recvbuf = dalloc<double2>(P, (size_t)std::max<int64_t>(1, X.recv_tot));
 }
 
+// Pivoted column selection of the HF directional sets on the device (plan.hpp Options::select).
+std::vector<int64_t> dev_select(const std::vector<std::array<double, 3>>& X, const std::vector<std::array<double, 3>>& Y,
+                                const std::vector<double>& rs, const std::vector<double>& cs, double k, double tol,
+                                int64_t maxrank) {
+  const int64_t m = (int64_t)X.size(), n = (int64_t)Y.size();
+  std::vector<int64_t> piv(std::min<int64_t>({m, n, maxrank}) + 1);
+  int64_t np = 0;
+  double *dx, *dy, *drs = nullptr, *dcs = nullptr;
+  double2* A;
+  ck(cudaMalloc(&dx, 3 * m * sizeof(double)));
+  ck(cudaMalloc(&dy, 3 * n * sizeof(double)));
+  ck(cudaMalloc(&A, (size_t)m * n * sizeof(double2)));
+  ck(cudaMemcpy(dx, X.data(), 3 * m * sizeof(double), cudaMemcpyHostToDevice));
+  ck(cudaMemcpy(dy, Y.data(), 3 * n * sizeof(double), cudaMemcpyHostToDevice));
+  if (!rs.empty()) {
+    ck(cudaMalloc(&drs, m * sizeof(double)));
+    ck(cudaMemcpy(drs, rs.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (!cs.empty()) {
+    ck(cudaMalloc(&dcs, n * sizeof(double)));
+    ck(cudaMemcpy(dcs, cs.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  fda::launch_gmat(A, dx, m, dy, n, drs, dcs, k, 0);
+  const cudaError_t e = fda::pivoted_columns(A, m, n, tol, maxrank, piv.data(), &np, 0);
+  for (void* p : {(void*)dx, (void*)dy, (void*)A, (void*)drs, (void*)dcs})
+    if (p) cudaFree(p);
+  ck(e);
+  piv.resize(np);
+  return piv;
+}
+
 bool finite3(const std::vector<double>& v) {
   for (double x : v)
     if (!std::isfinite(x)) return false;
@@ -836,6 +1021,13 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     if (o.hf_max_rows > 0) fo.hf_max_rows = o.hf_max_rows;
     if (o.hf_spacing > 0) fo.hf_spacing = o.hf_spacing;
     fo.verbose = o.verbose;
+    if (!o.host_only) {
+      // operators and HF directional sets on the device (plan_dev.cu); host-only plans skip the operators
+      fo.dev_ops = true;
+      fo.select = dev_select;
+    } else {
+      fo.dev_ops = true;  // host-only plans (list audits) need no operators
+    }
     std::string err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo);
     if (err == "COINCIDENT_POINTS") return FDA_ERR_COINCIDENT_POINTS;
     if (!err.empty()) return FDA_ERR_INVALID_ARG;
@@ -858,6 +1050,7 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     P->st.setup_upload_s = now() - t0;
     P->st.device_bytes = P->bytes;
     P->logstr = P->H.log;
+    if (o.verbose) P->logstr += fda::level_summary(P->H);
     // the host copies of the big pools are no longer needed
     std::vector<std::vector<cplx>>().swap(P->H.m2l_pool);
     for (auto& T : P->H.trans) std::vector<cplx>().swap(T.pool), std::vector<cplx>().swap(T.poolT);

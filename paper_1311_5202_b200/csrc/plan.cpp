@@ -124,6 +124,38 @@ static std::vector<P3> surface_grid(int p, double side) {
   return s;
 }
 
+// ------------------------------------------------------------------ point sets of a slot direction
+std::vector<std::array<double, 3>> dir_points(const Level& L, int d, bool check) {
+  if (!L.hf) return check ? L.ck_pts : L.eq_pts;
+  const DirRep& D = L.reps[L.dir_rep[d]];
+  std::vector<std::array<double, 3>> v;
+  for (const auto& p : check ? D.ap : D.bp) v.push_back(apply_sym(L.dir_sym[d], p));
+  return v;
+}
+
+// ------------------------------------------------------------------ per-level summary (plan log)
+std::string level_summary(const HostPlan& P) {
+  std::ostringstream log;
+  const double lambda = P.k > 0 ? 2.0 * PI / P.k : INFINITY;
+  for (size_t l = 0; l < P.levels.size(); ++l) {
+    const Level& L = P.levels[l];
+    int64_t npairs = 0, ngrp = 0, nlow = 0;
+    double fl = 0, rsum = 0;
+    for (auto& G : P.m2l_groups)
+      if (G.level == (int)l) {
+        const double np = (double)(G.pend - G.pbeg);
+        npairs += G.pend - G.pbeg, ++ngrp, nlow += G.rank >= 0;
+        fl += np * (G.rank < 0 ? 8.0 * L.s * L.s : 16.0 * G.rank * L.s);
+        rsum += np * (G.rank < 0 ? L.s : G.rank);
+      }
+    log << "  L" << l << " w/lambda=" << (P.k > 0 ? L.w / lambda : 0) << (L.hf ? " HF" : " LF") << " R=" << L.R
+        << " m=" << L.m << " cubes=" << L.cubes.size() << " s=" << L.s << " out=" << L.n_out << " in=" << L.n_in
+        << " m2l_pairs=" << npairs << " groups=" << ngrp << " lowrank=" << nlow
+        << " mean_rank=" << (npairs ? rsum / (double)npairs : 0.0) << " m2l_gflop=" << fl * 1e-9 << "\n";
+  }
+  return log.str();
+}
+
 // ------------------------------------------------------------------ build
 std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nrm, const double* w, double k,
                        cplx alpha, double eps, const Options& opt) {
@@ -483,6 +515,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       }
   }
 
+  const double tslots = now();
   // ---- P3: operators.  LF surfaces.
   const double eps_int = P.eps_int;
   for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
@@ -506,6 +539,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     L.s = (int)sv.s.size();
   }
 
+  const double tlf = now();
   // ---- P3: HF directional sets, top-down (R16)
   const std::vector<Sym> syms = all_syms();
   for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
@@ -568,7 +602,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     const int span = (int)std::min<int64_t>(2 * Rp + 1, (1LL << l) - 1);
     const bool parent_slots = (l - 1 >= lmin) && P.levels[l - 1].hf && !P.levels[l - 1].reps.empty();
     std::string err;
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) if (!opt.select)
     for (int ri = 0; ri < (int)repdirs.size(); ++ri) {
       const int rd = repdirs[ri];
       std::vector<P3> rows;
@@ -603,16 +637,27 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
         std::shuffle(rows.begin(), rows.end(), rng);
         rows.resize(opt.hf_max_rows);
       }
-      Mat A = Gmat(k, rows, cand);
-      for (int64_t i = 0; i < A.m; ++i) {
-        const double rr = std::sqrt(rows[i][0] * rows[i][0] + rows[i][1] * rows[i][1] + rows[i][2] * rows[i][2]);
-        for (int64_t j = 0; j < A.n; ++j) A(i, j) *= rr;
+      // A[i, j] = G(row_i, cand_j) |row_i|: columns J (equivalent points) by pivoted QR of A, then rows I
+      // (check points) by pivoted QR of A(:, J)^T
+      std::vector<double> rr(rows.size());
+      for (size_t i = 0; i < rows.size(); ++i)
+        rr[i] = std::sqrt(rows[i][0] * rows[i][0] + rows[i][1] * rows[i][1] + rows[i][2] * rows[i][2]);
+      std::vector<int64_t> J, I;
+      if (opt.select) {
+        J = opt.select(rows, cand, rr, {}, k, eps_int, 2000);
+        std::vector<std::array<double, 3>> cJ;
+        for (int64_t j : J) cJ.push_back(cand[j]);
+        I = opt.select(cJ, rows, {}, rr, k, eps_int, 2000);  // G symmetric: A(:, J)^T = G(cand_J, rows) |rows|
+      } else {
+        Mat A = Gmat(k, rows, cand);
+        for (int64_t i = 0; i < A.m; ++i)
+          for (int64_t j = 0; j < A.n; ++j) A(i, j) *= rr[i];
+        J = pivoted_qr(A, eps_int, 2000);
+        Mat AJt((int64_t)J.size(), A.m);
+        for (int64_t i = 0; i < A.m; ++i)
+          for (size_t t = 0; t < J.size(); ++t) AJt((int64_t)t, i) = A(i, J[t]);
+        I = pivoted_qr(AJt, eps_int, 2000);
       }
-      std::vector<int64_t> J = pivoted_qr(A, eps_int, 2000);
-      Mat AJt((int64_t)J.size(), A.m);
-      for (int64_t i = 0; i < A.m; ++i)
-        for (size_t t = 0; t < J.size(); ++t) AJt((int64_t)t, i) = A(i, J[t]);
-      std::vector<int64_t> I = pivoted_qr(AJt, eps_int, 2000);
       DirRep& D = L.reps[ri];
       D.dir = rd;
       for (int64_t j : J) D.bp.push_back(cand[j]);
@@ -655,6 +700,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   auto lv_eq = [&](const Level& L, int d) { return L.hf ? hf_b(L, d) : L.eq_pts; };
   auto lv_ck = [&](const Level& L, int d) { return L.hf ? hf_a(L, d) : L.ck_pts; };
 
+  const double thf = now();
   // ---- M2M / L2L matrices per transition (PAPER.md eq_cmpm / eq_cmpl: L~ = M~^T)
   for (int lp = std::max(lmin, 0); lmin >= 0 && lp + 1 < nlev; ++lp) {
     Level& Lp = P.levels[lp];
@@ -704,9 +750,14 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       T.dn_ptr[s + 1] = (int64_t)T.dn_parent.size();
     }
     const int64_t msz = (int64_t)T.sp * T.sc;
+    for (size_t t = 0; t < need.size(); ++t) T.mat_index[need[t].first * 8 + need[t].second] = (int64_t)t;
+    T.need = need;
+    if (opt.dev_ops) {  // built on the device (plan_dev.cu)
+      P.trans.push_back(std::move(T));
+      continue;
+    }
     T.pool.assign(need.size() * msz, cplx(0));
     T.poolT.assign(need.size() * msz, cplx(0));
-    for (size_t t = 0; t < need.size(); ++t) T.mat_index[need[t].first * 8 + need[t].second] = (int64_t)t;
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t t = 0; t < (int64_t)need.size(); ++t) {
       const int d = need[t].first, oc = need[t].second;
@@ -732,6 +783,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     P.trans.push_back(std::move(T));
   }
 
+  const double tm2m = now();
   // ---- M2L groups: K~ = U_dn^H K V_up = V^T G(delta + b_tgt, b_src) V   (eq_cmpk), low rank (eq_lrdk)
   P.m2l_pool.assign(nlev, {});
   for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
@@ -740,9 +792,10 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     const int64_t ng = (int64_t)lv_offs[l].size();
     if (!ng) continue;
     std::vector<std::vector<cplx>> gm(ng);
-    std::vector<int> grank(ng, -1);
-#pragma omp parallel for schedule(dynamic, 4)
+    std::vector<int> grank(ng, opt.dev_ops ? -2 : -1);
+#pragma omp parallel for schedule(dynamic, 4) if (!opt.dev_ops)
     for (int64_t g = 0; g < ng; ++g) {
+      if (opt.dev_ops) continue;  // K~ built on the device (plan_dev.cu)
       const int d = L.hf ? grp_dir[l][g] : 0;
       const int t = L.hf ? anti_dir(d, L.m) : 0;
       const double sh[3] = {-lv_offs[l][g][0] * L.w, -lv_offs[l][g][1] * L.w, -lv_offs[l][g][2] * L.w};
@@ -800,6 +853,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     }
   }
 
+  const double tm2l = now();
   // ---- S2M / L2T leaf operators per LF level (eq_cmps, eq_cmpt)
   for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
     Level& L = P.levels[l];
@@ -825,25 +879,12 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   }
   P.t_ops = now() - t0;
   if (opt.verbose) {
+    log << "ops: slots " << tslots - t0 << "s lf " << tlf - tslots << "s hf-sets " << thf - tlf << "s m2m " << tm2m - thf
+        << "s m2l " << tm2l - tm2m << "s leaf " << now() - tm2l << "s\n";
     log << "tree " << P.t_tree << "s lists " << P.t_lists << "s ops " << P.t_ops << "s; levels " << nlev
         << " leaves " << P.leaves.size() << " lmin " << lmin << "\n";
-    for (int l = 0; l < nlev; ++l) {
-      const Level& L = P.levels[l];
-      int64_t npairs = 0, ngrp = 0, nlow = 0;
-      double fl = 0, rsum = 0;
-      for (auto& G : P.m2l_groups)
-        if (G.level == l) {
-          const double np = (double)(G.pend - G.pbeg);
-          npairs += G.pend - G.pbeg, ++ngrp, nlow += G.rank >= 0;
-          fl += np * (G.rank < 0 ? 8.0 * L.s * L.s : 16.0 * G.rank * L.s);
-          rsum += np * (G.rank < 0 ? L.s : G.rank);
-        }
-      log << "  L" << l << " w/lambda=" << (k > 0 ? L.w / lambda : 0) << (L.hf ? " HF" : " LF") << " R=" << L.R
-          << " m=" << L.m << " cubes=" << L.cubes.size() << " s=" << L.s << " out=" << L.n_out << " in=" << L.n_in
-          << " m2l_pairs=" << npairs << " groups=" << ngrp << " lowrank=" << nlow
-          << " mean_rank=" << (npairs ? rsum / (double)npairs : 0.0) << " m2l_gflop=" << fl * 1e-9 << "\n";
-    }
     P.log = log.str();
+    if (!opt.dev_ops) P.log += level_summary(P);
   }
   return "";
 }

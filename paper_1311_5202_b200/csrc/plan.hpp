@@ -13,6 +13,7 @@
 #include <array>
 #include <complex>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -32,9 +33,16 @@ struct Options {
   int max_depth = 20;
   int hf_max_rows = 6000;   // HF interpolative-selection sample rows per direction representative
   double hf_spacing = 0.25; // HF candidate spacing in wavelengths
-  int64_t tgt_begin = 0;    // owned target points [tgt_begin, tgt_end) in Morton order (multi-GPU)
-  int64_t tgt_end = -1;
   int verbose = 0;
+  // Translation operators (M2M / L2L / M2L matrices) built on the device (plan_dev.cu) after the host plan:
+  // build_plan then only records which operators are needed (Trans::need, M2LGroup with rank = -2).
+  bool dev_ops = false;
+  // Pivoted column selection on A[i, j] = G(X_i - Y_j) rs_i cs_j (empty rs / cs: 1) with tolerance tol relative
+  // to the largest column, at most maxrank pivots (R16).  Empty: the host pivoted QR (linalg.cpp).
+  std::function<std::vector<int64_t>(const std::vector<std::array<double, 3>>& X,
+                                     const std::vector<std::array<double, 3>>& Y, const std::vector<double>& rs,
+                                     const std::vector<double>& cs, double k, double tol, int64_t maxrank)>
+      select;
 };
 
 struct Cube {
@@ -113,7 +121,7 @@ struct HostPlan {
     int off[3];
     int dir;          // source direction (HF) or 0
     int64_t pbeg, pend;  // into pair arrays
-    int rank;         // -1: dense K~, else low-rank rank r
+    int rank;         // -1: dense K~, else low-rank rank r; -2: not computed on the host (Options::dev_ops)
     int64_t mat_off;  // offset (complex elements) into the M2L matrix pool of the level
   };
   std::vector<M2LGroup> m2l_groups;
@@ -130,6 +138,7 @@ struct HostPlan {
     std::vector<int64_t> up_ptr, up_child, up_mat;
     // L2L: per child in slot CSR of (parent in slot, matrix id)
     std::vector<int64_t> dn_ptr, dn_parent, dn_mat;
+    std::vector<std::pair<int, int>> need;  // matrix id -> (parent direction, child octant)
   };
   std::vector<Trans> trans;
   // S2M / L2T: per LF level, leaves (global leaf index) with their slots
@@ -149,6 +158,13 @@ struct HostPlan {
 // Returns "" on success, else an error message.
 std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nrm, const double* w,
                        double k, std::complex<double> alpha, double eps, const Options& opt);
+
+// equivalent (check = false) or check (check = true) points of direction d of a level, relative to the cube
+// centre (HF: the representative's set mapped by the direction's cube symmetry; LF: the surfaces)
+std::vector<std::array<double, 3>> dir_points(const Level& L, int d, bool check);
+
+// per-level summary lines of the plan log (sizes, M2L pairs, ranks, flops)
+std::string level_summary(const HostPlan& P);
 
 // direction helpers (face grid, R15)
 int face_dir(const double v[3], int m);

@@ -228,7 +228,7 @@ std::vector<double> frag_pool(GroupedPairs& G, const cplx* raw, int s_out, int s
 // Fragment-order size (doubles) of a group's operator: dense s_out x s_in, or V (r x s_in) then U (s_out x r).
 int64_t frag_size(int rank, int s_out, int s_in) {
   if (rank < 0) return (int64_t)(pad8(s_out) / 8) * (pad4(s_in) / 4) * 64;
-  return (int64_t)(pad8(rank) / 8) * (pad4(s_in) / 4) * 64 + (int64_t)(pad8(s_out) / 8) * (pad8(rank) / 8) * 64;
+  return (int64_t)(pad8(rank) / 8) * (pad4(s_in) / 4) * 64 + (int64_t)(pad8(s_out) / 8) * (pad8(rank) / 4) * 64;
 }
 
 // Work items of a grouped translation.  raw != nullptr: the groups' matrices are the host column-major pool
@@ -1021,13 +1021,11 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     if (o.hf_max_rows > 0) fo.hf_max_rows = o.hf_max_rows;
     if (o.hf_spacing > 0) fo.hf_spacing = o.hf_spacing;
     fo.verbose = o.verbose;
-    if (!o.host_only) {
-      // operators and HF directional sets on the device (plan_dev.cu); host-only plans skip the operators
-      fo.dev_ops = true;
-      fo.select = dev_select;
-    } else {
-      fo.dev_ops = true;  // host-only plans (list audits) need no operators
-    }
+    // operators and HF directional sets on the device (plan_dev.cu); host-only plans (list audits) skip the
+    // operators; FDA_HOST_OPS=1 builds them on the host (linalg.cpp) instead, for cross-checks
+    static const bool host_ops = getenv("FDA_HOST_OPS") && getenv("FDA_HOST_OPS")[0] == '1';
+    fo.dev_ops = o.host_only || !host_ops;
+    if (!o.host_only && !host_ops) fo.select = dev_select;
     std::string err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo);
     if (err == "COINCIDENT_POINTS") return FDA_ERR_COINCIDENT_POINTS;
     if (!err.empty()) return FDA_ERR_INVALID_ARG;

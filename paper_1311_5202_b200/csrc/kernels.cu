@@ -379,11 +379,32 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// TMA bulk reduction (SASS UBLKRED): dst[0 .. bytes/8) += src[...] in FP64, shared -> global, element-wise
+// atomic at L2; one instruction per output column instead of 2 s_out per-lane REDG atomics (the LSU issue
+// rate of those bounded the translations: ~1.3 cycles per lane and SM).
+__device__ __forceinline__ void bulk_red_f64(double2* gdst, const double2* ssrc, unsigned bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst), "r"(sa),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// one lane per column of the staged tile Ys (ld s_out) issues its bulk reduction into Y[out slot]
+__device__ __forceinline__ void bulk_issue_cols(double2* Y, const double2* Ys, const int* sOut, int s_out, int nb,
+                                                int lane) {
+  for (int c = lane; c < nb; c += 32) bulk_red_f64(Y + (int64_t)sOut[c] * s_out, Ys + c * s_out, (unsigned)s_out * 16u);
+  bulk_commit();
+}
+
 __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 + 4; }  // >= k, = 4 mod 8
 
 // One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem double2).
 // Work units (row tile, column group, k split) are spread over the CTA's warps.
 // mode 0: C into the smem tile Ts (ldt) (ksplit must be 1: shared-memory FP64 atomics are CAS loops);
+// mode 3: rows < s_out of C into the smem tile Ts (ldt = s_out), for a bulk reduction into Y (ksplit 1);
 // mode 1: Y[sOut[col]*s_out + row] += C (plain RMW; Y loaded before the k loop so the load latency
 //         overlaps the MMAs); mode 2: same with global atomics.
 template <int GT_P, int MODE, int GT_CT, bool ASM = false>
@@ -439,6 +460,8 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         const double im = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
         if (MODE == 0) {
           Ts[col * ldt + row] = make_double2(re, im);
+        } else if (MODE == 3) {
+          if (row < s_out) Ts[col * ldt + row] = make_double2(re, im);
         } else if (row < s_out && col < nb) {
           double2* y = Y + (int64_t)sOut[col] * s_out + row;
           if (MODE == 2) {
@@ -491,16 +514,18 @@ __device__ __forceinline__ void gt_stage_ct(int ct, const double* __restrict__ A
 // landed (cp.async), [D] between the low-rank stages.  The next chunk's gather is issued right after
 // [C] into the other buffer (NBUF = 2) or, with one buffer, after [D] (X is dead once T = V X) or
 // after the dense stage; pair indices are triple-buffered and fetched two chunks ahead.
-template <int GT_P, int NBUF, bool STAGE>
+template <int GT_P, int NBUF, bool STAGE, bool YB>
 __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __restrict__ X, double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
   const int s_in = T.s_in, s_out = T.s_out;
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;  // k tiles of the input, m tiles of the output
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
   double2* Ts = gsm2 + NBUF * GT_P * ldx;
+  // YB (atomic items): the chunk's output tile (GT_P columns of s_out), bulk-reduced into Y per column
+  double2* Ys = Ts + GT_P * ldt;
   // STAGE: the current group's fragment-order matrix block is copied (cp.async, contiguous) into shared
   // memory once per group and read from there by every chunk of the item
-  double* Ms = reinterpret_cast<double*>(Ts + GT_P * ldt);
+  double* Ms = reinterpret_cast<double*>(Ys + (YB ? GT_P * s_out : 0));
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];  // pair indices of chunks i, i+1, i+2 (mod 3)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // Persistent CTAs: CTA b walks the items item_order[b], item_order[b + G], ... (G = gridDim.x) as one
@@ -571,6 +596,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   __syncthreads();
   issue_x(0, 0);
   int xbuf = 0, ib = 0;
+  bool ypend = false;  // YB: a bulk reduction of Ys is in flight (issued by warp 0)
   while (valid(cur)) {
     Cur nx = cur;
     advance(nx);
@@ -588,6 +614,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     int ct1 = T.ct1;
     if (ct1 <= 0) ct1 = rt * (GT_P / 16) >= GT_W / 2 ? 2 : 1;
     cp_async_wait<0>();
+    if (YB && ypend && warp == 0) bulk_wait_read();  // the bulk engine has read the previous chunk's Ys
     __syncthreads();  // [C] X (and Ms) of this chunk visible; previous chunk finished everywhere
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
     const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
@@ -600,14 +627,28 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       if (has_next2) load_idx(ib2, n2);  // buffer ib2 held chunk i-1's indices (done at [C])
       const double* U = Mg + (size_t)rt * kin * 64;
       const int kt2 = (rank + 3) / 4;  // U is stored with pad8(r) columns; ceil(r/4) k tiles are non-zero
-      if (T.atomic) {
+      if (YB) {  // atomic items, mout >= GT_W (no k split)
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, Ts, ldt, Ys, s_out, nullptr, nullptr,
+                                    s_out, nb, 2 * rt);
+        fence_async_smem();
+        __syncthreads();
+        if (warp == 0) bulk_issue_cols(Y, Ys, sOut[ib], s_out, nb, lane);
+        ypend = true;
+      } else if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kt2);
         gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), U, mout,
                                     kt2, ks, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(U, mout, kt2, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
     } else {
-      if (T.atomic) {
+      if (YB) {
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, Mg, mout, kin, 1, xb, ldx, Ys, s_out, nullptr, nullptr,
+                                    s_out, nb);
+        fence_async_smem();
+        __syncthreads();
+        if (warp == 0) bulk_issue_cols(Y, Ys, sOut[ib], s_out, nb, lane);
+        ypend = true;
+      } else if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kin);
         gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), Mg,
                                     mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
@@ -626,6 +667,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     cur = nx, ib = ib1;
     if (NBUF == 2) xbuf ^= 1;
   }
+  if (YB && warp == 0) bulk_wait_all();
 }
 
 // Warp-specialised variant for items whose groups are all low rank (atomic items): warps 0-3 run the
@@ -636,7 +678,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
-template <int GT_P, bool STAGE>
+template <int GT_P, bool STAGE, bool YB>
 __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* __restrict__ X,
                                                       double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
@@ -645,7 +687,9 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   const int ldx = gt_ld(kin * 4), ldt = gt_ld(T.rmax8);
   double2* Xs = gsm2;
   double2* const T0 = gsm2 + GT_P * ldx;  // T double buffer: T0 (even chunks), T0 + GT_P ldt (odd)
-  double* Ms = reinterpret_cast<double*>(gsm2 + GT_P * ldx + 2 * GT_P * ldt);
+  // YB: the stage-2 output tile (GT_P columns of s_out), bulk-reduced into Y (one UBLKRED per column)
+  double2* Ys = T0 + 2 * GT_P * ldt;
+  double* Ms = reinterpret_cast<double*>(Ys + (YB ? GT_P * s_out : 0));
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool grpA = warp < GT_W / 2;  // stage-1 warps (and the gather); the rest run stage 2
@@ -696,6 +740,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   __syncthreads();
   if (grpA) issue_x(0);
   int64_t eb = -1, cb = 0;  // chunk of the stage-2 warps (i - 1); -1: none yet
+  bool ypend = false;       // YB: a bulk reduction of Ys is in flight (issued by warp GT_W/2)
   int i = 0;
   while (ea < e_end || eb >= 0) {
     const int ia = i % 3, ibb = (i + 2) % 3;  // index buffers of chunks i and i - 1
@@ -705,10 +750,11 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
       cp_async_wait<0>();
       named_bar(1, GT_T / 2);  // X of chunk i visible to the stage-1 warps
-      const int ct1 = (rt % 2 == 0) ? 2 : 1;  // units = rt x (4 / ct1): a multiple of the 4 stage-1 warps
+      const int ct1 = (rt % 2 == 0 && GT_P >= 16) ? 2 : 1;  // units = rt x (GT_P / 8 / ct1)
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
                                   0, 0, 0, GT_W / 2);
     }
+    (void)ia;
     if (!grpA && eb >= 0) {
       // stage 2 of chunk i-1 on warps 4-7 (static units: letting the stage-1 warps claim stage-2 units
       // from a shared counter measured slower -- 312 vs 300 ms at config 5, more L2 traffic)
@@ -718,8 +764,19 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const double* U = Mg + (size_t)rt * kin * 64;
       const int kt2 = (rank + 3) / 4;
       const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
-      gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
-                                  nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+      if (YB) {
+        if (ypend && warp == GT_W / 2) bulk_wait_read();  // Ys of the previous chunk read by the bulk engine
+        named_bar(2, GT_T / 2);
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
+                                    Ys, s_out, nullptr, nullptr, s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+        fence_async_smem();
+        named_bar(2, GT_T / 2);
+        if (warp == GT_W / 2) bulk_issue_cols(Y, Ys, sOut[ibb], s_out, nb, lane);
+        ypend = true;
+      } else {
+        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
+                                    nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+      }
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
     // advance: stage 2 takes chunk i, stage 1 takes chunk i + 1
@@ -733,17 +790,26 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
     }
     ++i;
   }
+  if (YB && warp == GT_W / 2) bulk_wait_all();
 }
 
-static size_t gt_smem_ws(const GTrans& T, bool stage) {
+static size_t gt_smem_ws(const GTrans& T, int p, bool stage, bool yb) {
   const int kin = (T.s_in + 3) / 4;
-  return (size_t)(32 * gt_ld(kin * 4) + 2 * 32 * gt_ld(T.rmax8)) * sizeof(double2) +
+  return (size_t)(p * gt_ld(kin * 4) + 2 * p * gt_ld(T.rmax8) + (yb ? p * T.s_out : 0)) * sizeof(double2) +
          (stage ? (size_t)T.mmax * sizeof(double) : 0);
 }
+// bulk-reduced outputs (FDA_GT_BULK=0: per-lane FP64 atomics as in round 1)
+static bool gt_bulk() {
+  static const bool on = !(getenv("FDA_GT_BULK") && getenv("FDA_GT_BULK")[0] == '0');
+  return on;
+}
+static bool gt_yb(const GTrans& T) { return gt_bulk() && T.atomic && (T.s_out + 7) / 8 >= GT_W; }
 
+// bulk-reduced outputs apply to atomic items whose output has >= GT_W row tiles (no k split)
+static bool gt_yb(const GTrans& T);
 static size_t gt_smem(const GTrans& T, int p, int nbuf, bool stage) {
   const int kin = (T.s_in + 3) / 4;
-  return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8)) * sizeof(double2) +
+  return (size_t)(nbuf * p * gt_ld(kin * 4) + p * gt_ld(T.rmax8) + (gt_yb(T) ? p * T.s_out : 0)) * sizeof(double2) +
          (stage ? (size_t)T.mmax * sizeof(double) : 0);
 }
 // opt-in shared-memory limit per CTA of the current device (227 KB on B200)
@@ -796,10 +862,11 @@ int gtrans_cols(const GTrans& T) {
   return p;
 }
 
-template <int P, int NB, bool STG>
-static cudaError_t gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+template <int P, int NB, bool STG, bool YB>
+static cudaError_t gt_launch_k(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_gtrans<P, NB, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_gtrans<P, NB, STG, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
   // One CTA per item (the hardware block scheduler keeps the resident items a compact window of the
@@ -811,29 +878,37 @@ static cudaError_t gt_launch(const GTrans& T, const double2* X, double2* Y, size
     int dev = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gtrans<P, NB, STG>, GT_T, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gtrans<P, NB, STG, YB>, GT_T, sm);
     grid = std::min<int64_t>(T.n_items, (int64_t)std::max(1, per_sm) * nsm);
   }
-  k_gtrans<P, NB, STG><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
+  k_gtrans<P, NB, STG, YB><<<(unsigned)grid, GT_T, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
+template <int P, int NB, bool STG>
+static cudaError_t gt_launch(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
+  return gt_yb(T) ? gt_launch_k<P, NB, STG, true>(T, X, Y, sm, st) : gt_launch_k<P, NB, STG, false>(T, X, Y, sm, st);
+}
 
-// largest pad8 rank for which the warp-specialised kernel (32 columns, X + 2 T tiles) fits the budget
+// largest pad8 rank for which the warp-specialised kernel (16 columns, X + 2 T tiles + the bulk output tile)
+// fits the two-CTAs-per-SM budget
 int gtrans_ws_rmax(int s_in) {
   const int kin = (s_in + 3) / 4;
   int best = 0;
   for (int r8 = 8; r8 <= 512; r8 += 8)
-    if ((size_t)(32 * gt_ld(kin * 4) + 2 * 32 * gt_ld(r8)) * sizeof(double2) <= (size_t)GT_SMEM_BUDGET) best = r8;
+    if ((size_t)(16 * gt_ld(kin * 4) + 2 * 16 * gt_ld(r8) + (gt_bulk() ? 16 * s_in : 0)) * sizeof(double2) <=
+        (size_t)GT_SMEM_BUDGET)
+      best = r8;
   return best;
 }
 
-template <bool STG>
+template <int P, bool STG, bool YB>
 static cudaError_t gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_gtrans_ws<32, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_gtrans_ws<P, STG, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_gtrans_ws<32, STG><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  k_gtrans_ws<P, STG, YB><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
 
@@ -844,8 +919,22 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
   if (ws_ok && T.atomic && T.all_lowrank) {
     static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
                                                            : (size_t)GT_SMEM_BUDGET;
-    if (gt_smem_ws(T, true) <= budget) return gt_launch_ws<true>(T, X, Y, gt_smem_ws(T, true), st);
-    if (gt_smem_ws(T, false) <= budget) return gt_launch_ws<false>(T, X, Y, gt_smem_ws(T, false), st);
+    // FDA_GT_WSP=32|16: chunk width of the warp-specialised kernel (default: the widest that keeps two CTAs
+    // per SM; 32 columns with bulk outputs may take one CTA per SM with FDA_GT_WSP=32)
+    static const int wsp = getenv("FDA_GT_WSP") ? atoi(getenv("FDA_GT_WSP")) : 0;
+    const bool yb = gt_bulk();
+    for (int p : {32, 16}) {
+      if (wsp && p != wsp) continue;
+      const size_t lim = wsp == p ? smem_optin() : budget;
+      for (bool stg : {true, false}) {
+        const size_t sm = gt_smem_ws(T, p, stg, yb);
+        if (sm > lim) continue;
+        if (p == 32 && stg) return yb ? gt_launch_ws<32, true, true>(T, X, Y, sm, st) : gt_launch_ws<32, true, false>(T, X, Y, sm, st);
+        if (p == 32) return yb ? gt_launch_ws<32, false, true>(T, X, Y, sm, st) : gt_launch_ws<32, false, false>(T, X, Y, sm, st);
+        if (stg) return yb ? gt_launch_ws<16, true, true>(T, X, Y, sm, st) : gt_launch_ws<16, true, false>(T, X, Y, sm, st);
+        return yb ? gt_launch_ws<16, false, true>(T, X, Y, sm, st) : gt_launch_ws<16, false, false>(T, X, Y, sm, st);
+      }
+    }
   }
   int p, nb;
   bool stg;

@@ -739,7 +739,16 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       for (int o = 0; o < 8; ++o)
         if (Pc.child[o] >= 0 && P.cubes[Pc.child[o]].local == C.local && P.cubes[Pc.child[o]].level == C.level) oc = o;
       const int dc = Lc.in_dir[s];
-      for (int d = 0; d < Lp.ndir; ++d) {
+      // parent directions d with cdir(d) == dc: all of them for an LF child; for an HF child the 2 x 2 cells
+      // (f, 2a + i, 2b + j) of the parent's finer face grid that nest in the child's cell (f, a, b)
+      int cand[4], ncand = 0;
+      if (Lc.hf) {
+        const int mc = Lc.m, f = dc / (mc * mc), a = (dc % (mc * mc)) / mc, b = dc % mc, mp = Lp.m;
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) cand[ncand++] = (f * mp + 2 * a + i) * mp + 2 * b + j;
+      }
+      for (int q = 0; q < (Lc.hf ? ncand : Lp.ndir); ++q) {
+        const int d = Lc.hf ? cand[q] : q;
         if (cdir(d) != dc) continue;
         const int64_t ps = Lp.in_slot[Pc.local * Lp.ndir + d];
         if (ps < 0) continue;

@@ -123,11 +123,15 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
     __syncthreads();
     int rank = -1, np_ = 0;
     if (J.compress) {
+      // the MGS works on a copy C of O (in the G workspace, free once T is built): O stays K~ for a dense group
+      double2* C = Gk;
+      for (int e = tid; e < sA * sB; e += OP_T) C[e] = O[e];
+      __syncthreads();
       // ---- pivoted MGS (re-orthogonalised) of O's columns, tol 0.1 eps_lr of the largest column norm
       for (int j = warp; j < sB; j += OP_W) {
         double s = 0;
-        for (int a = lane; a < sA; a += 32) s += O[a + (size_t)j * sA].x * O[a + (size_t)j * sA].x +
-                                                  O[a + (size_t)j * sA].y * O[a + (size_t)j * sA].y;
+        for (int a = lane; a < sA; a += 32) s += C[a + (size_t)j * sA].x * C[a + (size_t)j * sA].x +
+                                                  C[a + (size_t)j * sA].y * C[a + (size_t)j * sA].y;
         s = wsum(s);
         if (lane == 0) nrm[j] = s;
       }
@@ -145,13 +149,13 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
         if (warp == 0) {
           double s = 0;
           for (int a = lane; a < sA; a += 32) {
-            const double2 v = O[a + (size_t)jb * sA];
+            const double2 v = C[a + (size_t)jb * sA];
             s += v.x * v.x + v.y * v.y;
           }
           s = wsum(s);
           const double inv = 1.0 / sqrt(s);
           for (int a = lane; a < sA; a += 32) {
-            const double2 v = O[a + (size_t)jb * sA];
+            const double2 v = C[a + (size_t)jb * sA];
             Q[a + (size_t)t * sA] = make_double2(v.x * inv, v.y * inv);
           }
           if (lane == 0) piv[t] = jb, used[jb] = 1;
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
             if (lane == 0) W[j + (size_t)t * sB] = make_double2(0.0, 0.0);  // W = R^H
             continue;
           }
-          double2* aj = O + (size_t)j * sA;
+          double2* aj = C + (size_t)j * sA;
           double2 tot = make_double2(0.0, 0.0);
           for (int pass2 = 0; pass2 < 2; ++pass2) {
             double2 c = make_double2(0.0, 0.0);

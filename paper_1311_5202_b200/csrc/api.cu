@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -15,6 +16,7 @@
 #include "nccl_dl.hpp"
 #include "plan.hpp"
 #include "plan_dev.cuh"
+#include "tree_dev.cuh"
 
 using fda::cplx;
 
@@ -62,8 +64,8 @@ struct fda_plan_s {
   int64_t bytes = 0;
   // geometry
   int64_t n = 0, nleaf = 0;
-  double *px, *py, *pz, *nx, *ny, *nz, *w;
-  int32_t* perm;
+  double *px = nullptr, *py = nullptr, *pz = nullptr, *nx = nullptr, *ny = nullptr, *nz = nullptr, *w = nullptr;
+  int32_t* perm = nullptr;
   int64_t* leaf_ptr;
   double *lcx, *lcy, *lcz;
   int64_t *p2p_ptr;
@@ -514,10 +516,12 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   fda::HostPlan& H = P->H;
   const int64_t n = H.n;
   P->n = n;
-  P->px = upload(P, H.px), P->py = upload(P, H.py), P->pz = upload(P, H.pz);
-  P->nx = upload(P, H.nx), P->ny = upload(P, H.ny), P->nz = upload(P, H.nz);
-  P->w = upload(P, H.w);
-  P->perm = upload(P, H.perm);
+  if (!P->px) {  // host-built tree (the device tree leaves the Morton-ordered geometry in place)
+    P->px = upload(P, H.px), P->py = upload(P, H.py), P->pz = upload(P, H.pz);
+    P->nx = upload(P, H.nx), P->ny = upload(P, H.ny), P->nz = upload(P, H.nz);
+    P->w = upload(P, H.w);
+    P->perm = upload(P, H.perm);
+  }
   const int64_t nl = (int64_t)H.leaves.size();
   P->nleaf = nl;
   std::vector<int64_t> lp(nl + 1);
@@ -552,6 +556,15 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     if (L.n_out) D.X = P->Xall + P->xoff[l];
     if (L.n_in) D.Y = dalloc<double2>(P, (size_t)L.n_in * L.s);
   }
+  std::ostringstream tlog;  // setup timings of the upload (plan log)
+  double tu = now();
+  auto lap = [&](const char* what) {
+    cudaDeviceSynchronize();
+    const double t = now();
+    tlog << what << " " << t - tu << "s ";
+    tu = t;
+  };
+  lap("geometry");
   // device point sets and factors of every level's directions (plan_dev.cuh DevSet), for the operators
   const bool dev_ops = H.opt.dev_ops;
   std::vector<std::vector<int>> bset(nlev), aset(nlev);
@@ -601,6 +614,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   auto set_max = [&](const std::vector<int>& ids, int* maxn) {
     for (int i : ids) *maxn = std::max(*maxn, P->dev_sets[i].n);
   };
+  lap("sets");
   // M2L: pairs filtered to owned targets, grouped by offset; operators built on the device
   for (int l = 0; l < nlev; ++l) {
     const fda::Level& L = H.levels[l];
@@ -693,6 +707,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
     }
   }
+  lap("m2l");
   // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
   // L2L items own child in slots (groups = the same matrices, transposed layout)
   for (const auto& T : H.trans) {
@@ -787,6 +802,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     P->st.flops_l2l += 0.5 * fdn;
     P->tr.push_back(D);
   }
+  lap("m2m/l2l");
   // leaf operators: S2M and L2T on this rank's leaves
   for (const auto& O : H.leafops) {
     const fda::Level& L = H.levels[O.level];
@@ -860,6 +876,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   s.owned_begin = P->pt_b, s.owned_end = P->pt_e;
   s.setup_tree_s = H.t_tree, s.setup_lists_s = H.t_lists, s.setup_ops_s = H.t_ops;
   upload_exchange(P);
+  lap("leaf/exchange");
+  if (o.verbose) P->H.log += "upload: " + tlog.str() + "\n";
   return FDA_OK;
 }
 
@@ -1002,12 +1020,15 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
   std::unique_ptr<fda_plan_s> P(new fda_plan_s());
   try {
     if (!o.host_only) cudaGetDevice(&P->dev);
-    std::vector<double> x = to_host(points, (size_t)n * 3), nr = to_host(normals, (size_t)n * 3),
-                        w = to_host(quad_weights, (size_t)n);
-    if (!finite3(x) || !finite3(nr) || !finite3(w)) return FDA_ERR_INVALID_ARG;
-    for (int64_t i = 0; i < n; ++i) {
-      const double nn = std::sqrt(nr[3 * i] * nr[3 * i] + nr[3 * i + 1] * nr[3 * i + 1] + nr[3 * i + 2] * nr[3 * i + 2]);
-      if (std::fabs(nn - 1.0) > 1e-10 || !(w[i] > 0)) return FDA_ERR_INVALID_ARG;
+    std::vector<double> x, nr, w;
+    const bool dev_tree = !o.host_only && !(getenv("FDA_HOST_TREE") && getenv("FDA_HOST_TREE")[0] == '1');
+    if (!dev_tree) {
+      x = to_host(points, (size_t)n * 3), nr = to_host(normals, (size_t)n * 3), w = to_host(quad_weights, (size_t)n);
+      if (!finite3(x) || !finite3(nr) || !finite3(w)) return FDA_ERR_INVALID_ARG;
+      for (int64_t i = 0; i < n; ++i) {
+        const double nn = std::sqrt(nr[3 * i] * nr[3 * i] + nr[3 * i + 1] * nr[3 * i + 1] + nr[3 * i + 2] * nr[3 * i + 2]);
+        if (std::fabs(nn - 1.0) > 1e-10 || !(w[i] > 0)) return FDA_ERR_INVALID_ARG;
+      }
     }
     fda::Options fo;
     fo.np = o.leaf_size;
@@ -1023,12 +1044,50 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     fo.verbose = o.verbose;
     // operators and HF directional sets on the device (plan_dev.cu); host-only plans (list audits) skip the
     // operators; FDA_HOST_OPS=1 builds them on the host (linalg.cpp) instead, for cross-checks
-    static const bool host_ops = getenv("FDA_HOST_OPS") && getenv("FDA_HOST_OPS")[0] == '1';
+    const bool host_ops = getenv("FDA_HOST_OPS") && getenv("FDA_HOST_OPS")[0] == '1';
     fo.dev_ops = o.host_only || !host_ops;
     if (!o.host_only && !host_ops) fo.select = dev_select;
-    std::string err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo);
-    if (err == "COINCIDENT_POINTS") return FDA_ERR_COINCIDENT_POINTS;
-    if (!err.empty()) return FDA_ERR_INVALID_ARG;
+    std::string err;
+    fda::TreeIn tin;
+    const double t_dev0 = now();
+    if (dev_tree) {
+      // rows a-P0 / a-P1 on the device (tree_dev.cu): validation, Morton sort, octree; the Morton-ordered
+      // geometry becomes the plan's
+      const double *dp = points, *dn = normals, *dw = quad_weights;
+      std::vector<void*> staged;
+      auto stage = [&](const double* h, size_t count) {
+        double* d = nullptr;
+        ck(cudaMalloc(&d, count * sizeof(double)));
+        staged.push_back(d);
+        ck(cudaMemcpy(d, h, count * sizeof(double), cudaMemcpyHostToDevice));
+        return (const double*)d;
+      };
+      if (!is_device_ptr(dp)) dp = stage(dp, (size_t)n * 3);
+      if (!is_device_ptr(dn)) dn = stage(dn, (size_t)n * 3);
+      if (!is_device_ptr(dw)) dw = stage(dw, (size_t)n);
+      fda_plan Pp = P.get();
+      Pp->px = dalloc<double>(Pp, n), Pp->py = dalloc<double>(Pp, n), Pp->pz = dalloc<double>(Pp, n);
+      Pp->nx = dalloc<double>(Pp, n), Pp->ny = dalloc<double>(Pp, n), Pp->nz = dalloc<double>(Pp, n);
+      Pp->w = dalloc<double>(Pp, n);
+      Pp->perm = dalloc<int32_t>(Pp, n);
+      const fda::DevGeom g{Pp->px, Pp->py, Pp->pz, Pp->nx, Pp->ny, Pp->nz, Pp->w, Pp->perm};
+      err = fda::build_tree_device(n, dp, dn, dw, k, fda::leaf_size_for(eps, fo.np), fo.single_leaf, fo.max_depth, g,
+                                   tin, 0);
+      for (void* p : staged) cudaFree(p);
+      if (err == "CUDA") throw CudaFail{FDA_ERR_CUDA};
+      if (!err.empty()) {
+        free_plan(Pp);
+        return err == "COINCIDENT_POINTS" ? FDA_ERR_COINCIDENT_POINTS : FDA_ERR_INVALID_ARG;
+      }
+    }
+    const double t_dev = now() - t_dev0;  // device P0 / P1 (with the input staging)
+    err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo,
+                          dev_tree ? &tin : nullptr);
+    P->H.t_tree += t_dev;
+    if (err == "COINCIDENT_POINTS" || !err.empty()) {
+      free_plan(P.get());
+      return err == "COINCIDENT_POINTS" ? FDA_ERR_COINCIDENT_POINTS : FDA_ERR_INVALID_ARG;
+    }
     P->host_only = o.host_only != 0;
     P->logstr = P->H.log;
     P->kind = o.kernel;
@@ -1089,41 +1148,42 @@ fda_status fda_plan_set_correction(fda_plan P, int64_t nnz, const int64_t* row_p
     double2* n_val = nullptr;
     int64_t own = 0;
     if (nnz > 0) {
-      // validate and permute into NEW buffers first: on any error the plan keeps its current correction
-      std::vector<int64_t> rp = to_host(row_ptr, (size_t)n + 1);
-      if (rp[0] != 0 || rp[n] != nnz) return FDA_ERR_INVALID_ARG;
-      for (int64_t i = 0; i < n; ++i)
-        if (rp[i + 1] < rp[i]) return FDA_ERR_INVALID_ARG;
-      std::vector<int32_t> cl = to_host(col, (size_t)nnz);
-      for (int64_t p = 0; p < nnz; ++p)
-        if (cl[p] < 0 || cl[p] >= n) return FDA_ERR_INVALID_ARG;
-      std::vector<double> vl = to_host(val, (size_t)nnz * 2);
-      // permute into Morton order: row m = caller row perm[m]; columns through the inverse permutation
-      const std::vector<int32_t>& perm = P->H.perm;
-      std::vector<int32_t> inv(n);
-      for (int64_t m = 0; m < n; ++m) inv[perm[m]] = (int32_t)m;
-      std::vector<int64_t> mp(n + 1, 0);
-      for (int64_t m = 0; m < n; ++m) mp[m + 1] = mp[m] + (rp[perm[m] + 1] - rp[perm[m]]);
-      // only this rank's rows are stored (a multi-GPU rank applies its own rows)
-      const int64_t o0 = mp[P->pt_b], o1 = mp[P->pt_e];
-      std::vector<int32_t> mc(o1 - o0);
-      std::vector<double> mv((size_t)(o1 - o0) * 2);
-#pragma omp parallel for schedule(dynamic, 1024)
-      for (int64_t m = P->pt_b; m < P->pt_e; ++m) {
-        const int64_t i = perm[m];
-        int64_t o = mp[m] - o0;
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p, ++o) {
-          mc[o] = inv[cl[p]];
-          mv[2 * o] = vl[2 * p];
-          mv[2 * o + 1] = vl[2 * p + 1];
+      // validate and permute on the device into NEW buffers first: on any error the plan keeps its current
+      // correction.  Host arrays are staged to the device.
+      std::vector<void*> staged;
+      auto stage = [&](const void* h, size_t bytes) -> const void* {
+        if (is_device_ptr(h)) return h;
+        void* d = nullptr;
+        ck(cudaMalloc(&d, bytes));
+        staged.push_back(d);
+        ck(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+        return d;
+      };
+      auto unstage = [&] {
+        for (void* p : staged) cudaFree(p);
+        staged.clear();
+      };
+      try {
+        const int64_t* drp = (const int64_t*)stage(row_ptr, (size_t)(n + 1) * sizeof(int64_t));
+        const int32_t* dcol = (const int32_t*)stage(col, (size_t)nnz * sizeof(int32_t));
+        const double2* dval = (const double2*)stage(val, (size_t)nnz * sizeof(double2));
+        n_ptr = dalloc<int64_t>(P, (size_t)n + 1);
+        const std::string err = fda::permute_csr_device(n, nnz, drp, dcol, dval, P->perm, P->pt_b, P->pt_e, n_ptr,
+                                                        &n_col, &n_val, &own, 0);
+        unstage();
+        if (err == "CUDA") throw CudaFail{FDA_ERR_CUDA};
+        if (!err.empty()) {
+          auto it = std::find(P->allocs.begin(), P->allocs.end(), (void*)n_ptr);
+          if (it != P->allocs.end()) P->allocs.erase(it);
+          cudaFree(n_ptr);
+          return FDA_ERR_INVALID_ARG;
         }
+        P->allocs.push_back(n_col), P->allocs.push_back(n_val);
+        P->bytes += own * (int64_t)(sizeof(int32_t) + sizeof(double2));
+      } catch (...) {
+        unstage();
+        throw;
       }
-      std::vector<double>().swap(vl);
-      for (auto& v : mp) v -= o0;
-      n_ptr = upload(P, mp);
-      n_col = upload(P, mc);
-      n_val = upload(P, reinterpret_cast<const double2*>(mv.data()), (size_t)(o1 - o0));
-      own = o1 - o0;
     }
     if (P->c_ptr) {  // release the old correction only now that the new one is in place
       for (void* p : {(void*)P->c_ptr, (void*)P->c_col, (void*)P->c_val}) {

@@ -889,13 +889,14 @@ static cudaError_t gt_launch(const GTrans& T, const double2* X, double2* Y, size
   return gt_yb(T) ? gt_launch_k<P, NB, STG, true>(T, X, Y, sm, st) : gt_launch_k<P, NB, STG, false>(T, X, Y, sm, st);
 }
 
-// largest pad8 rank for which the warp-specialised kernel (16 columns, X + 2 T tiles + the bulk output tile)
-// fits the two-CTAs-per-SM budget
+// largest pad8 rank for which the warp-specialised kernel fits the two-CTAs-per-SM budget: 32 columns with
+// per-lane atomic outputs, 16 columns with the bulk output tile
 int gtrans_ws_rmax(int s_in) {
   const int kin = (s_in + 3) / 4;
+  const int p = gt_bulk() ? 16 : 32;
   int best = 0;
   for (int r8 = 8; r8 <= 512; r8 += 8)
-    if ((size_t)(16 * gt_ld(kin * 4) + 2 * 16 * gt_ld(r8) + (gt_bulk() ? 16 * s_in : 0)) * sizeof(double2) <=
+    if ((size_t)(p * gt_ld(kin * 4) + 2 * p * gt_ld(r8) + (gt_bulk() ? p * s_in : 0)) * sizeof(double2) <=
         (size_t)GT_SMEM_BUDGET)
       best = r8;
   return best;

@@ -157,8 +157,22 @@ std::string level_summary(const HostPlan& P) {
 }
 
 // ------------------------------------------------------------------ build
+int leaf_size_for(double eps, int np_opt) {
+  return np_opt > 0 ? np_opt : (int)std::max(30.0, std::round(50.0 * (-std::log10(eps) - 3.0)));
+}
+
+static inline uint64_t compact3(uint64_t v) {  // inverse of spread3
+  v &= 0x1249249249249249ull;
+  v = (v | (v >> 2)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v >> 4)) & 0x100f00f00f00f00full;
+  v = (v | (v >> 8)) & 0x1f0000ff0000ffull;
+  v = (v | (v >> 16)) & 0x1f00000000ffffull;
+  v = (v | (v >> 32)) & 0x1fffff;
+  return v;
+}
+
 std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nrm, const double* w, double k,
-                       cplx alpha, double eps, const Options& opt) {
+                       cplx alpha, double eps, const Options& opt, const TreeIn* tin) {
   std::ostringstream log;
   double t0 = now();
   P.n = n;
@@ -171,102 +185,130 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
   P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 3.0;
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
-  P.np = opt.np > 0 ? opt.np : (int)std::max(30.0, std::round(50.0 * (-std::log10(eps) - 3.0)));
+  P.np = leaf_size_for(eps, opt.np);
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;
 
-  // ---- P0: bounding cube, Morton sort
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t i = 0; i < n; ++i)
-    for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], x[3 * i + d]), hi[d] = std::max(hi[d], x[3 * i + d]);
-  double W = 0;
-  for (int d = 0; d < 3; ++d) W = std::max(W, hi[d] - lo[d]);
-  if (W <= 0) W = 1.0;
-  W *= (1.0 + 1e-6);  // root = bounding cube x (1 + 1e-6)   (R13)
-  double ctr[3];
-  for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]), P.root_lo[d] = ctr[d] - 0.5 * W;
-  P.root_w = W;
-  std::vector<uint64_t> key(n);
-  const double scale = (double)(1 << MAXD) / W;
-#pragma omp parallel for
-  for (int64_t i = 0; i < n; ++i) {
-    uint64_t c[3];
-    for (int d = 0; d < 3; ++d) {
-      double u = (x[3 * i + d] - P.root_lo[d]) * scale;
-      int64_t v = (int64_t)std::floor(u);
-      v = std::min<int64_t>(std::max<int64_t>(v, 0), (1 << MAXD) - 1);
-      c[d] = (uint64_t)v;
-    }
-    key[i] = morton(c[0], c[1], c[2]);
-  }
-  std::vector<int32_t> ord(n);
-  std::iota(ord.begin(), ord.end(), 0);
-  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-  P.perm = ord;
-  P.px.resize(n), P.py.resize(n), P.pz.resize(n), P.nx.resize(n), P.ny.resize(n), P.nz.resize(n), P.w.resize(n);
-  std::vector<uint64_t> skey(n);
-  for (int64_t t = 0; t < n; ++t) {
-    const int64_t i = ord[t];
-    P.px[t] = x[3 * i], P.py[t] = x[3 * i + 1], P.pz[t] = x[3 * i + 2];
-    P.nx[t] = nrm[3 * i], P.ny[t] = nrm[3 * i + 1], P.nz[t] = nrm[3 * i + 2];
-    P.w[t] = w[i];
-    skey[t] = key[i];
-  }
-  // coincident points -> error
-  for (int64_t t = 1; t < n; ++t) {
-    if (skey[t] == skey[t - 1]) {
-      const double dx = P.px[t] - P.px[t - 1], dy = P.py[t] - P.py[t - 1], dz = P.pz[t] - P.pz[t - 1];
-      if (std::sqrt(dx * dx + dy * dy + dz * dz) < 1e-14 * W) return "COINCIDENT_POINTS";
-    }
-  }
-
-  // ---- P1: adaptive octree
+  std::vector<std::vector<int64_t>> bylevel;
+  double W = 1;
   auto level_w = [&](int l) { return W / (double)(1LL << l); };
   auto is_hf = [&](int l) { return k > 0 && level_w(l) >= lambda; };  // HF iff w >= lambda (R13)
-  P.cubes.clear();
-  {
-    Cube r{};
-    r.level = 0;
-    r.ijk[0] = r.ijk[1] = r.ijk[2] = 0;
-    r.pbeg = 0, r.pend = n, r.parent = -1;
-    for (auto& c : r.child) c = -1;
-    r.leaf = true;
-    P.cubes.push_back(r);
-  }
-  std::vector<std::vector<int64_t>> bylevel(1, std::vector<int64_t>{0});
-  for (int l = 0; l < opt.max_depth; ++l) {
-    std::vector<int64_t> next;
-    for (int64_t ci : bylevel[l]) {
-      Cube c = P.cubes[ci];
-      const int64_t cnt = c.pend - c.pbeg;
-      const bool split = !opt.single_leaf && (cnt > P.np || is_hf(l));
-      if (!split) continue;
-      P.cubes[ci].leaf = false;
-      const int shift = 3 * (MAXD - l - 1);
-      int64_t b = c.pbeg;
-      for (int oct = 0; oct < 8; ++oct) {
-        // first point with octant bits > oct
-        int64_t e = std::upper_bound(skey.begin() + b, skey.begin() + c.pend, (uint64_t)oct,
-                                     [&](uint64_t v, uint64_t kk) { return v < ((kk >> shift) & 7); }) -
-                    skey.begin();
-        if (e > b) {
-          Cube ch{};
-          ch.level = l + 1;
-          ch.ijk[0] = 2 * c.ijk[0] + ((oct >> 2) & 1);
-          ch.ijk[1] = 2 * c.ijk[1] + ((oct >> 1) & 1);
-          ch.ijk[2] = 2 * c.ijk[2] + (oct & 1);
-          ch.pbeg = b, ch.pend = e, ch.parent = ci;
-          for (auto& cc : ch.child) cc = -1;
-          ch.leaf = true;
-          const int64_t id = (int64_t)P.cubes.size();
-          P.cubes.push_back(ch);
-          P.cubes[ci].child[oct] = id;
-          next.push_back(id);
-        }
-        b = e;
+  if (tin) {
+    // P0 / P1 from the device (tree_dev.cu): cubes level-major, Morton order within a level
+    W = tin->root_w;
+    for (int d = 0; d < 3; ++d) P.root_lo[d] = tin->root_lo[d];
+    P.root_w = W;
+    P.perm = tin->perm;
+    const int64_t nc = (int64_t)tin->level.size();
+    P.cubes.resize(nc);
+    for (int64_t c = 0; c < nc; ++c) {
+      Cube& C = P.cubes[c];
+      C.level = tin->level[c];
+      const uint64_t kk = (uint64_t)tin->key[c];
+      C.ijk[0] = (int64_t)compact3(kk >> 2), C.ijk[1] = (int64_t)compact3(kk >> 1), C.ijk[2] = (int64_t)compact3(kk);
+      C.pbeg = tin->pbeg[c], C.pend = tin->pend[c], C.parent = tin->parent[c];
+      for (auto& ch : C.child) ch = -1;
+      C.leaf = tin->leaf[c] != 0;
+      if ((int)bylevel.size() <= C.level) bylevel.resize(C.level + 1);
+      bylevel[C.level].push_back(c);
+      if (C.parent >= 0) {
+        const Cube& Pp = P.cubes[C.parent];
+        const int oct = (int)(((C.ijk[0] - 2 * Pp.ijk[0]) << 2) | ((C.ijk[1] - 2 * Pp.ijk[1]) << 1) | (C.ijk[2] - 2 * Pp.ijk[2]));
+        P.cubes[C.parent].child[oct] = c;
       }
     }
-    if (next.empty()) break;
-    bylevel.push_back(std::move(next));
+  } else {
+    // ---- P0: bounding cube, Morton sort
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t i = 0; i < n; ++i)
+      for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], x[3 * i + d]), hi[d] = std::max(hi[d], x[3 * i + d]);
+    W = 0;
+    for (int d = 0; d < 3; ++d) W = std::max(W, hi[d] - lo[d]);
+    if (W <= 0) W = 1.0;
+    W *= (1.0 + 1e-6);  // root = bounding cube x (1 + 1e-6)   (R13)
+    double ctr[3];
+    for (int d = 0; d < 3; ++d) ctr[d] = 0.5 * (lo[d] + hi[d]), P.root_lo[d] = ctr[d] - 0.5 * W;
+    P.root_w = W;
+    std::vector<uint64_t> key(n);
+    const double scale = (double)(1 << MAXD) / W;
+#pragma omp parallel for
+    for (int64_t i = 0; i < n; ++i) {
+      uint64_t c[3];
+      for (int d = 0; d < 3; ++d) {
+        double u = (x[3 * i + d] - P.root_lo[d]) * scale;
+        int64_t v = (int64_t)std::floor(u);
+        v = std::min<int64_t>(std::max<int64_t>(v, 0), (1 << MAXD) - 1);
+        c[d] = (uint64_t)v;
+      }
+      key[i] = morton(c[0], c[1], c[2]);
+    }
+    std::vector<int32_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    P.perm = ord;
+    P.px.resize(n), P.py.resize(n), P.pz.resize(n), P.nx.resize(n), P.ny.resize(n), P.nz.resize(n), P.w.resize(n);
+    std::vector<uint64_t> skey(n);
+    for (int64_t t = 0; t < n; ++t) {
+      const int64_t i = ord[t];
+      P.px[t] = x[3 * i], P.py[t] = x[3 * i + 1], P.pz[t] = x[3 * i + 2];
+      P.nx[t] = nrm[3 * i], P.ny[t] = nrm[3 * i + 1], P.nz[t] = nrm[3 * i + 2];
+      P.w[t] = w[i];
+      skey[t] = key[i];
+    }
+    // coincident points -> error
+    for (int64_t t = 1; t < n; ++t) {
+      if (skey[t] == skey[t - 1]) {
+        const double dx = P.px[t] - P.px[t - 1], dy = P.py[t] - P.py[t - 1], dz = P.pz[t] - P.pz[t - 1];
+        if (std::sqrt(dx * dx + dy * dy + dz * dz) < 1e-14 * W) return "COINCIDENT_POINTS";
+      }
+    }
+  
+    // ---- P1: adaptive octree
+    P.cubes.clear();
+    {
+      Cube r{};
+      r.level = 0;
+      r.ijk[0] = r.ijk[1] = r.ijk[2] = 0;
+      r.pbeg = 0, r.pend = n, r.parent = -1;
+      for (auto& c : r.child) c = -1;
+      r.leaf = true;
+      P.cubes.push_back(r);
+    }
+    bylevel.assign(1, std::vector<int64_t>{0});
+    for (int l = 0; l < opt.max_depth; ++l) {
+      std::vector<int64_t> next;
+      for (int64_t ci : bylevel[l]) {
+        Cube c = P.cubes[ci];
+        const int64_t cnt = c.pend - c.pbeg;
+        const bool split = !opt.single_leaf && (cnt > P.np || is_hf(l));
+        if (!split) continue;
+        P.cubes[ci].leaf = false;
+        const int shift = 3 * (MAXD - l - 1);
+        int64_t b = c.pbeg;
+        for (int oct = 0; oct < 8; ++oct) {
+          // first point with octant bits > oct
+          int64_t e = std::upper_bound(skey.begin() + b, skey.begin() + c.pend, (uint64_t)oct,
+                                       [&](uint64_t v, uint64_t kk) { return v < ((kk >> shift) & 7); }) -
+                      skey.begin();
+          if (e > b) {
+            Cube ch{};
+            ch.level = l + 1;
+            ch.ijk[0] = 2 * c.ijk[0] + ((oct >> 2) & 1);
+            ch.ijk[1] = 2 * c.ijk[1] + ((oct >> 1) & 1);
+            ch.ijk[2] = 2 * c.ijk[2] + (oct & 1);
+            ch.pbeg = b, ch.pend = e, ch.parent = ci;
+            for (auto& cc : ch.child) cc = -1;
+            ch.leaf = true;
+            const int64_t id = (int64_t)P.cubes.size();
+            P.cubes.push_back(ch);
+            P.cubes[ci].child[oct] = id;
+            next.push_back(id);
+          }
+          b = e;
+        }
+      }
+      if (next.empty()) break;
+      bylevel.push_back(std::move(next));
+    }
   }
   const int nlev = (int)bylevel.size();
   P.levels.assign(nlev, Level());

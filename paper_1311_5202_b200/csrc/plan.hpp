@@ -154,14 +154,30 @@ struct HostPlan {
   std::string log;
 };
 
-// Build the plan.  x/nrm interleaved xyz (n x 3), w (n), all host, caller order.
+// P0 / P1 built on the device (tree_dev.cu): root box, Morton permutation and every cube, level-major
+// (the level's cubes in Morton order), as the host builder would number them.
+struct TreeIn {
+  double root_lo[3] = {0, 0, 0}, root_w = 1;
+  std::vector<int32_t> perm;                // Morton position -> caller index
+  std::vector<int> level;                   // per cube
+  std::vector<int64_t> key;                 // per cube: Morton prefix (3 bits per level)
+  std::vector<int64_t> pbeg, pend, parent;  // per cube (parent: global id, -1 for the root)
+  std::vector<unsigned char> leaf;
+};
+
+// Build the plan.  x/nrm interleaved xyz (n x 3), w (n), all host, caller order.  With tin (the device-built
+// tree) the host P0 / P1 are skipped and x / nrm / w are not read (the geometry stays on the device).
 // Returns "" on success, else an error message.
 std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nrm, const double* w,
-                       double k, std::complex<double> alpha, double eps, const Options& opt);
+                       double k, std::complex<double> alpha, double eps, const Options& opt,
+                       const TreeIn* tin = nullptr);
 
 // equivalent (check = false) or check (check = true) points of direction d of a level, relative to the cube
 // centre (HF: the representative's set mapped by the direction's cube symmetry; LF: the surfaces)
 std::vector<std::array<double, 3>> dir_points(const Level& L, int d, bool check);
+
+// N_p = max(30, 50 (-log10 eps - 3)) (eq_npleaf, sign-corrected; R12), or np_opt > 0
+int leaf_size_for(double eps, int np_opt);
 
 // per-level summary lines of the plan log (sizes, M2L pairs, ranks, flops)
 std::string level_summary(const HostPlan& P);

@@ -174,15 +174,11 @@ void free_plan(fda_plan P) {
 // Pairs (out slot, in slot) in group-major order; each group one translation matrix.
 struct GroupedPairs {
   std::vector<int64_t> gptr{0};
-  std::vector<int64_t> out, in;
+  std::vector<int32_t> out, in;
   std::vector<int32_t> rank;
   std::vector<int64_t> mat;
 };
 
-// Split the output slots into work items that own them exclusively (direction x Morton slab of
-// cubes), so the grouped-translation kernel accumulates without atomics; each item walks its
-// groups in order.  Slab count: enough pairs per (item, group) to amortise the matrix
-// (>= ~32) and enough items to fill the GPU (>= 2 CTAs per SM).
 // Append matrix A (M x K; element (i, j) = a(i, j)) in DMMA fragment order, padded to Mp x Kp
 // (kernels.cuh GTrans): tiles (mt, kt) of 8 x 4, each 32 real parts in lane order then 32 imaginary.
 template <class F>
@@ -264,14 +260,8 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     if (getenv("FDA_GT_CT2")) T.ct2 = atoi(getenv("FDA_GT_CT2"));
   }
   const int cols = fda::gtrans_cols(T);
-  std::unordered_map<int, int64_t> dix;
-  for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
-  const int64_t nd = (int64_t)dix.size();
   const double ppg = (double)np / (double)std::max<int64_t>(ng, 1);
-  // parallelism first (>= 8 items per SM), then ~2 chunks of pairs per (item, group) where the groups allow
-  int64_t S = std::max<int64_t>((int64_t)(ppg / (2 * cols)), (8 * 148 + nd - 1) / nd);
-  S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
-  // FDA_GT_MODE=atomic|owned forces the item kind (experiments); FDA_GT_CHUNK: pairs per atomic item
+  // FDA_GT_MODE=atomic|owned|auto forces the item kind (experiments); FDA_GT_CHUNK: pairs per atomic item
   const char* gm = getenv("FDA_GT_MODE");
   // Default: group-major items of <= 1024 pairs with atomic accumulation (measured at config 5: 400 ms
   // apply vs 440 ms with the automatic choice and 509 ms with owned items only; 1024 vs 256 pairs:
@@ -281,6 +271,16 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
                             ? std::max(1, atoi(getenv("FDA_GT_CHUNK")))
                             : std::max<int64_t>(32, std::min<int64_t>(1024, (np / (16 * 148) + 31) / 32 * 32));
   const bool force_owned = gm && !strcmp(gm, "owned"), use_auto = gm && !strcmp(gm, "auto");
+  // owned items: (output direction) x (Morton slab of cubes); parallelism first (>= 8 items per SM), then
+  // ~2 chunks of pairs per (item, group) where the groups allow
+  std::unordered_map<int, int64_t> dix;
+  int64_t S = 1;
+  if (force_owned || use_auto) {
+    for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
+    const int64_t nd = (int64_t)dix.size();
+    S = std::max<int64_t>((int64_t)(ppg / (2 * cols)), (8 * 148 + nd - 1) / nd);
+    S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
+  }
   if (!force_owned && (!use_auto || ppg / (double)S < 0.75 * cols)) {
     // Few pairs per group: owned items would reload each matrix for ~1 pair.  Group-major items
     // (chunks of <= 128 pairs of one group) reuse the matrix; outputs then need atomics.
@@ -296,7 +296,8 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
         cost.push_back((double)(q - p) * (r < 0 ? (double)s_out * s_in : (double)r * (s_out + s_in)));
         order.push_back((int32_t)order.size());
       }
-    std::vector<int32_t> pout(G.out.begin(), G.out.end()), pin(G.in.begin(), G.in.end());
+    const std::vector<int32_t>& pout = G.out;
+    const std::vector<int32_t>& pin = G.in;
     // Launch order: by the first output slot of the item (pairs of a group are sorted by output slot,
     // slots are numbered in Morton order), so the items resident at any time cover a narrow Morton
     // window of targets -- their y rows and nearby x rows stay in L2 -- across all groups.
@@ -320,7 +321,7 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     T.s_out = s_out, T.s_in = s_in, T.atomic = 1;
     return T;
   }
-  const int64_t nitems = nd * S;
+  const int64_t nitems = (int64_t)dix.size() * S;
   std::vector<int64_t> item(np);
   std::vector<int64_t> cnt(nitems + 1, 0);
   for (int64_t p = 0; p < np; ++p) {
@@ -618,23 +619,37 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   // M2L: pairs filtered to owned targets, grouped by offset; operators built on the device
   for (int l = 0; l < nlev; ++l) {
     const fda::Level& L = H.levels[l];
+    // groups of the level with pairs into this rank's target cubes, counted in parallel, then filled in
+    // parallel (group-major, pairs in the plan's order)
+    std::vector<int64_t> lg;  // group indices of the level
+    for (size_t gi = 0; gi < H.m2l_groups.size(); ++gi)
+      if (H.m2l_groups[gi].level == l) lg.push_back((int64_t)gi);
+    std::vector<int64_t> cntg(lg.size(), 0);
+    auto keep_pair = [&](int64_t p) { return R == 1 || owned_cube(L.cubes[L.in_cube[H.m2l_tgt[p]]]); };
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t q = 0; q < (int64_t)lg.size(); ++q) {
+      const auto& g = H.m2l_groups[lg[q]];
+      int64_t c = 0;
+      for (int64_t p = g.pbeg; p < g.pend; ++p) c += keep_pair(p);
+      cntg[q] = c;
+    }
     GroupedPairs G;
     std::vector<int64_t> gid;  // group index in H.m2l_groups
-    for (size_t gi = 0; gi < H.m2l_groups.size(); ++gi) {
-      const auto& g = H.m2l_groups[gi];
-      if (g.level != l) continue;
-      const size_t b0 = G.out.size();
-      for (int64_t p = g.pbeg; p < g.pend; ++p) {
-        const int64_t ts = H.m2l_tgt[p];
-        if (R > 1 && !owned_cube(L.cubes[L.in_cube[ts]])) continue;
-        G.out.push_back(ts);
-        G.in.push_back(H.m2l_src[p]);
-      }
-      if (G.out.size() == b0) continue;
-      G.gptr.push_back((int64_t)G.out.size());
+    for (size_t q = 0; q < lg.size(); ++q) {
+      if (!cntg[q]) continue;
+      const auto& g = H.m2l_groups[lg[q]];
+      G.gptr.push_back(G.gptr.back() + cntg[q]);
       G.rank.push_back(g.rank);
       G.mat.push_back(g.mat_off);
-      gid.push_back((int64_t)gi);
+      gid.push_back(lg[q]);
+    }
+    G.out.resize(G.gptr.back()), G.in.resize(G.gptr.back());
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t g = 0; g < (int64_t)gid.size(); ++g) {
+      const auto& hg = H.m2l_groups[gid[g]];
+      int64_t o = G.gptr[g];
+      for (int64_t p = hg.pbeg; p < hg.pend; ++p)
+        if (keep_pair(p)) G.out[o] = (int32_t)H.m2l_tgt[p], G.in[o] = (int32_t)H.m2l_src[p], ++o;
     }
     if (G.out.empty()) continue;
     const double* dpool = nullptr;
@@ -693,14 +708,33 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     // the nearest offsets) go to a second launch of the general kernel.
     const int rlim = fda::gtrans_ws_rmax(L.s);
     GroupedPairs G1, G2;
-    for (size_t g = 0; g < G.rank.size(); ++g) {
-      GroupedPairs& D = (G.rank[g] >= 0 && G.rank[g] <= rlim) ? G1 : G2;
-      for (int64_t q = G.gptr[g]; q < G.gptr[g + 1]; ++q) D.out.push_back(G.out[q]), D.in.push_back(G.in[q]);
-      D.gptr.push_back((int64_t)D.out.size());
-      D.rank.push_back(G.rank[g]);
-      D.mat.push_back(G.mat[g]);
+    {
+      std::vector<char> in1(G.rank.size());
+      for (size_t g = 0; g < G.rank.size(); ++g) {
+        in1[g] = G.rank[g] >= 0 && G.rank[g] <= rlim;
+        GroupedPairs& D = in1[g] ? G1 : G2;
+        D.gptr.push_back(D.gptr.back() + (G.gptr[g + 1] - G.gptr[g]));
+        D.rank.push_back(G.rank[g]);
+        D.mat.push_back(G.mat[g]);
+      }
+      if (!G1.rank.empty() && !G2.rank.empty()) {
+        G1.out.resize(G1.gptr.back()), G1.in.resize(G1.gptr.back());
+        G2.out.resize(G2.gptr.back()), G2.in.resize(G2.gptr.back());
+        std::vector<int64_t> dst(G.rank.size());
+        int64_t o1 = 0, o2 = 0;
+        for (size_t g = 0; g < G.rank.size(); ++g) {
+          dst[g] = in1[g] ? o1 : o2;
+          (in1[g] ? o1 : o2) += G.gptr[g + 1] - G.gptr[g];
+        }
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t g = 0; g < (int64_t)G.rank.size(); ++g) {
+          GroupedPairs& D = in1[g] ? G1 : G2;
+          std::copy(G.out.begin() + G.gptr[g], G.out.begin() + G.gptr[g + 1], D.out.begin() + dst[g]);
+          std::copy(G.in.begin() + G.gptr[g], G.in.begin() + G.gptr[g + 1], D.in.begin() + dst[g]);
+        }
+      }
     }
-    if (!G1.out.empty() && !G2.out.empty()) {
+    if (!G1.rank.empty() && !G2.rank.empty()) {
       P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
       P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
     } else {
@@ -732,8 +766,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
         for (int64_t e = ptr[s]; e < ptr[s + 1]; ++e) {
           if (!keep(s, other[e])) continue;
           const int64_t pos = fill[T.mat_index[mat[e]]]++;
-          G.out[pos] = s;
-          G.in[pos] = other[e];
+          G.out[pos] = (int32_t)s;
+          G.in[pos] = (int32_t)other[e];
         }
       for (int64_t g = 0; g < nmat; ++g) {
         G.gptr.push_back(cnt[g + 1]);
@@ -819,9 +853,9 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     D.surf = upload(P, sf);
     {  // S2M reduction: pairs (out = leaf slot, in = owned-leaf row t of the check-potential buffer)
       GroupedPairs G;
-      G.out = so_;
+      G.out.assign(so_.begin(), so_.end());
       G.in.resize(lo_.size());
-      for (size_t t = 0; t < lo_.size(); ++t) G.in[t] = (int64_t)t;
+      for (size_t t = 0; t < lo_.size(); ++t) G.in[t] = (int32_t)t;
       G.gptr.push_back((int64_t)G.out.size());
       G.rank.push_back(-1);
       G.mat.push_back(0);
@@ -829,10 +863,10 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     }
     {  // L2T reduction: pairs (out = owned-leaf row t, in = leaf slot)
       GroupedPairs G;
-      G.in = so_;
+      G.in.assign(so_.begin(), so_.end());
       G.out.resize(lo_.size());
       std::vector<int64_t> oc(lo_.size());
-      for (size_t t = 0; t < lo_.size(); ++t) G.out[t] = (int64_t)t, oc[t] = L.in_cube[so_[t]];
+      for (size_t t = 0; t < lo_.size(); ++t) G.out[t] = (int32_t)t, oc[t] = L.in_cube[so_[t]];
       std::vector<int> od(lo_.size(), 0);
       G.gptr.push_back((int64_t)G.out.size());
       G.rank.push_back(-1);

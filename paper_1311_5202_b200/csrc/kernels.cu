@@ -798,9 +798,13 @@ static size_t gt_smem_ws(const GTrans& T, int p, bool stage, bool yb) {
   return (size_t)(p * gt_ld(kin * 4) + 2 * p * gt_ld(T.rmax8) + (yb ? p * T.s_out : 0)) * sizeof(double2) +
          (stage ? (size_t)T.mmax * sizeof(double) : 0);
 }
-// bulk-reduced outputs (FDA_GT_BULK=0: per-lane FP64 atomics as in round 1)
+// bulk-reduced outputs (FDA_GT_BULK=1; default: per-lane FP64 atomics).  Measured at config 5 (round 2,
+// FDA_TRACE per-level times): the TMA bulk reduction is slower than the REDG atomics on every level
+// (LF M2L 151 vs 114 ms with the 16-column tile it needs for two CTAs per SM, 163 ms with 32 columns and
+// one CTA per SM; HF levels +8%), so the reduction payload at L2, not the SM-side atomic issue, bounds
+// the accumulation.
 static bool gt_bulk() {
-  static const bool on = !(getenv("FDA_GT_BULK") && getenv("FDA_GT_BULK")[0] == '0');
+  static const bool on = getenv("FDA_GT_BULK") && getenv("FDA_GT_BULK")[0] == '1';
   return on;
 }
 static bool gt_yb(const GTrans& T) { return gt_bulk() && T.atomic && (T.s_out + 7) / 8 >= GT_W; }

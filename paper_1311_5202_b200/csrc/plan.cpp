@@ -884,6 +884,8 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       grank[g] = rank;
     }
     std::vector<cplx>& pool = P.m2l_pool[l];
+    const int64_t pair0 = (int64_t)P.m2l_tgt.size(), grp0 = (int64_t)P.m2l_groups.size();
+    int64_t npl = 0;
     for (int64_t g = 0; g < ng; ++g) {
       HostPlan::M2LGroup G;
       G.level = l;
@@ -892,16 +894,26 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       G.rank = grank[g];
       G.mat_off = (int64_t)pool.size();
       pool.insert(pool.end(), gm[g].begin(), gm[g].end());
-      G.pbeg = (int64_t)P.m2l_tgt.size();
-      const int t = L.hf ? anti_dir(G.dir, L.m) : 0;
-      for (const PairL& pr : lv_pairs[l][g]) {
-        P.m2l_tgt.push_back(L.in_slot[(int64_t)pr.b * L.ndir + t]);
-        P.m2l_src.push_back(L.out_slot[(int64_t)pr.c * L.ndir + G.dir]);
-      }
-      G.pend = (int64_t)P.m2l_tgt.size();
-      P.m2l_groups.push_back(G);
       std::vector<cplx>().swap(gm[g]);
+      G.pbeg = pair0 + npl;
+      npl += (int64_t)lv_pairs[l][g].size();
+      G.pend = pair0 + npl;
+      P.m2l_groups.push_back(G);
     }
+    P.m2l_tgt.resize(pair0 + npl), P.m2l_src.resize(pair0 + npl);
+    // pairs -> (target in slot, source out slot), in parallel over the level's groups
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t g = 0; g < ng; ++g) {
+      const HostPlan::M2LGroup& G = P.m2l_groups[grp0 + g];
+      const int t = L.hf ? anti_dir(G.dir, L.m) : 0;
+      int64_t o = G.pbeg;
+      for (const PairL& pr : lv_pairs[l][g]) {
+        P.m2l_tgt[o] = L.in_slot[(int64_t)pr.b * L.ndir + t];
+        P.m2l_src[o] = L.out_slot[(int64_t)pr.c * L.ndir + G.dir];
+        ++o;
+      }
+    }
+    std::vector<std::vector<PairL>>().swap(lv_pairs[l]);
   }
 
   const double tm2l = now();

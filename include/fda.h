@@ -85,9 +85,9 @@ typedef enum {
 typedef struct {
   int32_t leaf_size;       /* N_p; 0 -> max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected) */
   double eps_internal;     /* expansion truncation (R+ SVDs, HF interpolative selection); 0 -> eps / 100 (R11) */
-  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch; 0 (default) -> 6 + dp with
-                              dp = round(log10(1e-4 / eps)) for eps < 1e-4, else 0 (R17); a value > 1 is
-                              used verbatim */
+  int32_t lf_p_low;        /* LF surface points per cube edge below lf_p_switch; 0 (default) -> 6 + dp (7 + dp
+                              below w = lambda / 4) with dp = round(log10(1e-4 / eps)) for eps < 1e-4, else 0
+                              (R17); a value > 1 is used verbatim */
   int32_t lf_p_high;       /* ... at or above lf_p_switch wavelengths; 0 (default) -> 8 + dp */
   double lf_p_switch;      /* w / lambda switch (default 0.75) */
   int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */
@@ -97,7 +97,7 @@ typedef struct {
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1);
                               nranks <= 64; see fda_plan_create_dist / fda_apply_up */
   int32_t verbose;         /* plan log (fda_plan_log) */
-  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
+  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 30 (R23) */
   int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
                               FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat);
                               FDA_KERNEL_T1: K = G + alpha dG/dn_y (eq_sum; Table 1 mode,

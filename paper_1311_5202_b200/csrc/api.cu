@@ -177,6 +177,7 @@ struct GroupedPairs {
   std::vector<int32_t> out, in;
   std::vector<int32_t> rank;
   std::vector<int64_t> mat;
+  std::vector<int16_t> so, si;  // optional: the group's own output / input expansion lengths
 };
 
 // Append matrix A (M x K; element (i, j) = a(i, j)) in DMMA fragment order, padded to Mp x Kp
@@ -318,6 +319,7 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     T.in = upload(P, pin);
     T.grank = upload(P, G.rank);
     T.gmat = upload(P, G.mat);
+    if (!G.so.empty()) T.gso = upload(P, G.so), T.gsi = upload(P, G.si);
     T.s_out = s_out, T.s_in = s_in, T.atomic = 1;
     return T;
   }
@@ -641,6 +643,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       G.gptr.push_back(G.gptr.back() + cntg[q]);
       G.rank.push_back(g.rank);
       G.mat.push_back(g.mat_off);
+      G.so.push_back((int16_t)L.sdir(L.hf ? fda::anti_dir(g.dir, L.m) : 0));
+      G.si.push_back((int16_t)L.sdir(g.dir));
       gid.push_back(lg[q]);
     }
     G.out.resize(G.gptr.back()), G.in.resize(G.gptr.back());
@@ -716,6 +720,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
         D.gptr.push_back(D.gptr.back() + (G.gptr[g + 1] - G.gptr[g]));
         D.rank.push_back(G.rank[g]);
         D.mat.push_back(G.mat[g]);
+        D.so.push_back(G.so[g]), D.si.push_back(G.si[g]);
       }
       if (!G1.rank.empty() && !G2.rank.empty()) {
         G1.out.resize(G1.gptr.back()), G1.in.resize(G1.gptr.back());
@@ -776,6 +781,13 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       }
       return G;
     };
+    // the (parent direction, child direction) expansion lengths of every M2M matrix
+    auto sizes = [&](GroupedPairs& G, bool up) {
+      for (int64_t g = 0; g < nmat; ++g) {
+        const int d = T.need[g].first, sp_ = Lp.sdir(Lp.hf ? d : 0), sc_ = Lc.sdir(Lc.hf ? fda::child_dir(d, Lp.m) : 0);
+        G.so.push_back((int16_t)(up ? sp_ : sc_)), G.si.push_back((int16_t)(up ? sc_ : sp_));
+      }
+    };
     // multi-GPU: M2M only from child cubes with points of this rank (partial sums); L2L only
     // into child cubes with points of this rank (their local expansions are complete here)
     double fup = 0, fdn = 0;  // algorithmic flops with the directions' own expansion lengths
@@ -820,6 +832,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     }
     if (!T.up_child.empty()) {
       GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat, up_keep);
+      sizes(G, true);
       if (dev_ops)
         for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sp, T.sc);
       D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc,
@@ -827,6 +840,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     }
     if (!T.dn_parent.empty()) {
       GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat, dn_keep);
+      sizes(G, false);
       if (dev_ops)
         for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sc, T.sp);
       D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp,

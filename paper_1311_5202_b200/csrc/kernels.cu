@@ -465,8 +465,12 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         } else if (row < s_out && col < nb) {
           double2* y = Y + (int64_t)sOut[col] * s_out + row;
           if (MODE == 2) {
-            atomicAdd(&y->x, re);
-            atomicAdd(&y->y, im);
+            // rows past the group's own expansion length (an HF wedge shorter than the level's padded s)
+            // are exact zeros: no atomic for them
+            if (re != 0.0 || im != 0.0) {
+              atomicAdd(&y->x, re);
+              atomicAdd(&y->y, im);
+            }
           } else {
             *y = make_double2(yv[c][i].x + re, yv[c][i].y + im);
           }
@@ -570,13 +574,18 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
       sIn[ib][tid] = v ? T.in[p] : -1;
     }
   };
-  auto issue_x = [&](int xbuf, int ib) {  // warp per pair column, lanes along k (no division)
+  // per-group expansion lengths (HF wedges are shorter than the level's padded s; their tails are zero):
+  // k tiles of the input / row tiles of the output actually used, and the gathered length
+  auto kin_of = [&](int grp) { return T.gsi ? (T.gsi[grp] + 3) / 4 : kin; };
+  auto mout_of = [&](int grp) { return T.gso ? (T.gso[grp] + 7) / 8 : mout; };
+  auto issue_x = [&](int xbuf, int ib, int grp) {  // warp per pair column, lanes along k (no division)
     double2* xb = gsm2 + xbuf * GT_P * ldx;
+    const int len = min(4 * kin_of(grp), s_in);
     for (int c = warp; c < GT_P; c += GT_W) {
       const int src = sIn[ib][c];
       if (src < 0) continue;
       const double2* xs = X + (int64_t)src * s_in;
-      for (int k = lane; k < s_in; k += 32) cp_async16(xb + c * ldx + k, xs + k);
+      for (int k = lane; k < len; k += 32) cp_async16(xb + c * ldx + k, xs + k);
     }
     cp_async_commit();
   };
@@ -594,7 +603,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
   if (valid(c1)) load_idx(1, c1);
   if (STAGE) stage_m(T.ig_group[cur.e]);
   __syncthreads();
-  issue_x(0, 0);
+  issue_x(0, 0, T.ig_group[cur.e]);
   int xbuf = 0, ib = 0;
   bool ypend = false;  // YB: a bulk reduction of Ys is in flight (issued by warp 0)
   while (valid(cur)) {
@@ -619,16 +628,17 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
     const int nb = (int)min((int64_t)GT_P, T.ig_pe[e] - c0);
     const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
     const double2* xb = gsm2 + xbuf * GT_P * ldx;
-    if (NBUF == 2 && has_next) issue_x(xbuf ^ 1, ib1);  // the other buffer was last read by chunk i-1
+    const int kin_g = T.atomic ? kin_of(grp) : kin, mout_g = T.atomic ? mout_of(grp) : mout;
+    if (NBUF == 2 && has_next) issue_x(xbuf ^ 1, ib1, T.ig_group[nx.e]);  // the other buffer was last read by chunk i-1
     if (rank >= 0) {
-      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0);
+      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin_g, 1, xb, ldx, Ts, ldt, nullptr, nullptr, 0, 0, kin);
       __syncthreads();  // [D] T complete, X of this chunk no longer read
-      if (NBUF == 1 && has_next) issue_x(0, ib1);
+      if (NBUF == 1 && has_next) issue_x(0, ib1, T.ig_group[nx.e]);
       if (has_next2) load_idx(ib2, n2);  // buffer ib2 held chunk i-1's indices (done at [C])
       const double* U = Mg + (size_t)rt * kin * 64;
       const int kt2 = (rank + 3) / 4;  // U is stored with pad8(r) columns; ceil(r/4) k tiles are non-zero
       if (YB) {  // atomic items, mout >= GT_W (no k split)
-        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, Ts, ldt, Ys, s_out, nullptr, nullptr,
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, Ts, ldt, Ys, s_out, nullptr, nullptr,
                                     s_out, nb, 2 * rt);
         fence_async_smem();
         __syncthreads();
@@ -636,28 +646,28 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
         ypend = true;
       } else if (T.atomic) {
         const int ks = gt_ksplit_y(mout, kt2);
-        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), U, mout,
+        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), U, mout_g,
                                     kt2, ks, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(U, mout, kt2, 1, Ts, ldt, nullptr, 0, Y, sOut[ib], s_out, nb, 2 * rt);
     } else {
       if (YB) {
-        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, Mg, mout, kin, 1, xb, ldx, Ys, s_out, nullptr, nullptr,
-                                    s_out, nb);
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, Mg, mout_g, kin_g, 1, xb, ldx, Ys, s_out, nullptr,
+                                    nullptr, s_out, nb, kin);
         fence_async_smem();
         __syncthreads();
         if (warp == 0) bulk_issue_cols(Y, Ys, sOut[ib], s_out, nb, lane);
         ypend = true;
       } else if (T.atomic) {
-        const int ks = gt_ksplit_y(mout, kin);
+        const int ks = gt_ksplit_y(mout, kin_g);
         gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : (T.ct2 < 0 ? gt_pick_ct<GT_P>(mout, ks) : GT_P / 8), Mg,
-                                    mout, kin, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
+                                    mout_g, kin_g, ks, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb, kin);
       } else
         gt_stage<GT_P, 1, 2, STAGE>(Mg, mout, kin, 1, xb, ldx, nullptr, 0, Y, sOut[ib], s_out, nb);
       if (has_next2) load_idx(ib2, n2);
       if (NBUF == 1 && has_next) {
         __syncthreads();  // X buffer free
-        issue_x(0, ib1);
+        issue_x(0, ib1, T.ig_group[nx.e]);
       }
     }
     if (STAGE && has_next && T.ig_group[nx.e] != grp) {
@@ -713,17 +723,20 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       sIn[ib][tid] = v ? T.in[p] : -1;
     }
   };
+  // all groups of an atomic item are one group; stage its matrix once (all threads)
+  const int grp0 = T.ig_group[e_beg];
+  // the group's own expansion lengths (HF wedges shorter than the level's padded s; their tails are zero)
+  const int kin_g = T.gsi ? (T.gsi[grp0] + 3) / 4 : kin, mout_g = T.gso ? (T.gso[grp0] + 7) / 8 : mout;
+  const int xlen = min(4 * kin_g, s_in);
   auto issue_x = [&](int ib) {  // by the stage-1 warps
     for (int c = warp; c < GT_P; c += GT_W / 2) {
       const int src = sIn[ib][c];
       if (src < 0) continue;
       const double2* xs = X + (int64_t)src * s_in;
-      for (int k = lane; k < s_in; k += 32) cp_async16(Xs + c * ldx + k, xs + k);
+      for (int k = lane; k < xlen; k += 32) cp_async16(Xs + c * ldx + k, xs + k);
     }
     cp_async_commit();
   };
-  // all groups of an atomic item are one group; stage its matrix once (all threads)
-  const int grp0 = T.ig_group[e_beg];
   if (STAGE) {
     const int rank = T.grank[grp0], rt = (rank + 7) / 8;
     const double* src = T.pool + T.gmat[grp0];
@@ -751,8 +764,8 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       cp_async_wait<0>();
       named_bar(1, GT_T / 2);  // X of chunk i visible to the stage-1 warps
       const int ct1 = (rt % 2 == 0 && GT_P >= 16) ? 2 : 1;  // units = rt x (GT_P / 8 / ct1)
-      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
-                                  0, 0, 0, GT_W / 2);
+      gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin_g, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
+                                  0, kin, 0, GT_W / 2);
     }
     (void)ia;
     if (!grpA && eb >= 0) {
@@ -767,15 +780,15 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       if (YB) {
         if (ypend && warp == GT_W / 2) bulk_wait_read();  // Ys of the previous chunk read by the bulk engine
         named_bar(2, GT_T / 2);
-        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
-                                    Ys, s_out, nullptr, nullptr, s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+        gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt,
+                                    ldt, Ys, s_out, nullptr, nullptr, s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
         fence_async_smem();
         named_bar(2, GT_T / 2);
         if (warp == GT_W / 2) bulk_issue_cols(Y, Ys, sOut[ibb], s_out, nb, lane);
         ypend = true;
       } else {
-        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt, ldt,
-                                    nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt,
+                                    ldt, nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
       }
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free

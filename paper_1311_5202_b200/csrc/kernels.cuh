@@ -62,6 +62,8 @@ struct GTrans {
   const int32_t* grank = nullptr;       // group -> -1 (dense) or r
   const int64_t* gmat = nullptr;        // group -> matrix offset (doubles) into pool
   const double* pool = nullptr;         // fragment-order matrices
+  const int16_t* gso = nullptr;         // group -> its own output / input expansion length (<= s_out / s_in;
+  const int16_t* gsi = nullptr;         //   the rest of the padded operator is zero); null: s_out / s_in
   int s_out = 0, s_in = 0, rmax8 = 0;   // rmax8: largest low rank rounded up to 8
   int64_t mmax = 0;                     // largest matrix block of a group (doubles): shared-memory staging
   int all_lowrank = 0;                  // every group low rank (warp-specialised kernel)

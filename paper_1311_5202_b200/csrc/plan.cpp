@@ -183,7 +183,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   // DESIGN.md R11 / R23: expansion truncation (R+, HF interpolative selection) at eps_int, low-rank M2L
   // truncation at eps_lr (measured: the low-rank cut contributes no visible error at eps_int)
   P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
-  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 3.0;
+  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 30.0;
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
   P.np = leaf_size_for(eps, opt.np);
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;
@@ -567,8 +567,11 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     // one more surface point per edge for each decade of eps below 1e-4 (measured: the LF surface
     // resolution caps the accuracy below 1e-4, profiles/r01_eps_probe.jsonl; unchanged at eps >= 1e-4)
     const int dp = eps < 1e-4 ? (int)std::lround(std::log10(1e-4 / eps)) : 0;
-    // explicit lf_p_low / lf_p_high options are used verbatim; the eps bump applies to the defaults only
-    const int p_low = opt.lf_p_low > 0 ? opt.lf_p_low : 6 + dp, p_high = opt.lf_p_high > 0 ? opt.lf_p_high : 8 + dp;
+    // explicit lf_p_low / lf_p_high options are used verbatim; the eps bump applies to the defaults only.
+    // Default p: 6 for 0.25 <= w/lambda < 0.75, 7 below 0.25 (the low-frequency levels: measured far-field
+    // error 2.4e-3 with p = 6 against 5.8e-4 with p = 7 at kD = 1, profiles/r02_far_probe_c2.jsonl), 8 above.
+    const int p_low = opt.lf_p_low > 0 ? opt.lf_p_low : (wl < 0.25 ? 7 : 6) + dp;
+    const int p_high = opt.lf_p_high > 0 ? opt.lf_p_high : 8 + dp;
     L.p = wl < opt.lf_p_switch ? p_low : p_high;
     L.eq_pts = surface_grid(L.p, 1.05 * L.w);  // outgoing equivalent = incoming check (inner)
     L.ck_pts = surface_grid(L.p, 2.95 * L.w);  // outgoing check = incoming equivalent (outer)

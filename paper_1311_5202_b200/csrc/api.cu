@@ -92,6 +92,8 @@ struct fda_plan_s {
   ncclComm_t comm = nullptr;  // fda_plan_create_dist
   cudaStream_t xstream = nullptr;
   cudaEvent_t ev_up = nullptr, ev_x = nullptr;
+  cudaStream_t nstream = nullptr;  // near field (P2P, correction), concurrent with the far field
+  cudaEvent_t ev_perm = nullptr, ev_near = nullptr;
   // correction
   int64_t nnz = 0;
   int64_t* c_ptr = nullptr;
@@ -1132,8 +1134,9 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     err = fda::build_plan(P->H, n, x.data(), nr.data(), w.data(), k, cplx(alpha_re, alpha_im), eps, fo,
                           dev_tree ? &tin : nullptr);
     P->H.t_tree += t_dev;
-    if (err == "COINCIDENT_POINTS" || !err.empty()) {
+    if (!err.empty()) {
       free_plan(P.get());
+      if (err == "SETUP_ACCURACY") return FDA_ERR_SETUP_ACCURACY;
       return err == "COINCIDENT_POINTS" ? FDA_ERR_COINCIDENT_POINTS : FDA_ERR_INVALID_ARG;
     }
     P->host_only = o.host_only != 0;
@@ -1151,6 +1154,9 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
       free_plan(P.get());
       return s;
     }
+    ck(cudaStreamCreateWithFlags(&P->nstream, cudaStreamNonBlocking));
+    ck(cudaEventCreateWithFlags(&P->ev_perm, cudaEventDisableTiming));
+    ck(cudaEventCreateWithFlags(&P->ev_near, cudaEventDisableTiming));
     ck(cudaDeviceSynchronize());
     P->st.setup_upload_s = now() - t0;
     P->st.device_bytes = P->bytes;
@@ -1291,15 +1297,18 @@ fda::LeafGeom leaves_of(fda_plan P) { return fda::LeafGeom{P->leaf_ptr, P->lcx, 
 double2 alpha_of(fda_plan P) { return make_double2(P->H.alpha.real(), P->H.alpha.imag()); }
 bool has_far(fda_plan P, uint32_t mask) { return (mask & FDA_PHASE_FAR) && P->H.lmin >= 0; }
 
-// H1 + upward pass (H4 S2M on this rank's leaves, H5 M2M on cubes with this rank's points) + pack of the
-// partial expansions other ranks need into sendbuf
-void stage_up(fda_plan P, uint32_t mask, const double2* d_phi, double2* sendbuf, cudaStream_t st, Marks& mk,
-              Trace& tr) {
-  const fda::Points Pt = points_of(P);
-  const fda::LeafGeom Lg = leaves_of(P);
+// H1: q = w phi, phi and q in Morton order
+void stage_permute(fda_plan P, const double2* d_phi, cudaStream_t st, Marks& mk) {
   mk.begin(0);
   fda::launch_permute_scale(P->n, P->perm, P->w, d_phi, P->q, P->phim, st);
   mk.end(0);
+}
+
+// upward pass (H4 S2M on this rank's leaves, H5 M2M on cubes with this rank's points) + pack of the
+// partial expansions other ranks need into sendbuf
+void stage_up(fda_plan P, uint32_t mask, double2* sendbuf, cudaStream_t st, Marks& mk, Trace& tr) {
+  const fda::Points Pt = points_of(P);
+  const fda::LeafGeom Lg = leaves_of(P);
   if (!has_far(P, mask)) return;
   mk.begin(3);
   // M2M accumulates into the non-leaf slots: clear every level's outgoing expansions first
@@ -1338,7 +1347,8 @@ void stage_near(fda_plan P, uint32_t mask, cudaStream_t st, Marks& mk) {
 }
 
 // unpack of the received partial expansions, then H6 M2L, H7 L2L, H8 L2T into this rank's rows
-void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t st, Marks& mk, Trace& tr) {
+void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t st, Marks& mk, Trace& tr,
+                cudaEvent_t near_done = nullptr) {
   if (!has_far(P, mask)) return;
   const fda::Points Pt = points_of(P);
   const fda::LeafGeom Lg = leaves_of(P);
@@ -1360,6 +1370,7 @@ void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t 
   }
   mk.end(6);
   mk.begin(7);
+  if (near_done) ck(cudaStreamWaitEvent(st, near_done, 0));  // L2T adds into the rows P2P / CSR wrote
   for (const auto& O : P->lo) {
     ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
     ck(fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st));
@@ -1455,23 +1466,33 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
     if (mk.on)
       for (auto& e : mk.ev) ck(cudaEventCreate(&e));
     Trace tr;
-    stage_up(P, mask, d_phi, P->xc.sendbuf, st, mk, tr);
+    stage_permute(P, d_phi, st, mk);
     const bool xchg = P->nranks > 1 && has_far(P, mask);
+    // the near field (P2P, correction: H2, H3) runs on the plan's side stream, concurrent with the far
+    // field; L2T (which adds into the same rows) waits for it.  Timed applies run the phases in sequence.
+    const bool overlap = !mk.on && !tr.on && has_far(P, mask);
+    if (overlap) {
+      ck(cudaEventRecord(P->ev_perm, st));
+      ck(cudaStreamWaitEvent(P->nstream, P->ev_perm, 0));
+      stage_near(P, mask, P->nstream, mk);
+      ck(cudaEventRecord(P->ev_near, P->nstream));
+    }
+    stage_up(P, mask, P->xc.sendbuf, st, mk, tr);
     if (xchg && !mk.on) {
-      // the exchange runs on the plan's side stream while P2P and the correction run here
+      // the exchange runs on the plan's exchange stream
       ck(cudaEventRecord(P->ev_up, st));
       ck(cudaStreamWaitEvent(P->xstream, P->ev_up, 0));
       nccl_exchange(P, P->xstream);
       ck(cudaEventRecord(P->ev_x, P->xstream));
-      stage_near(P, mask, st, mk);
+      if (!overlap) stage_near(P, mask, st, mk);
       ck(cudaStreamWaitEvent(st, P->ev_x, 0));
     } else {
       mk.begin(9);
       if (xchg) nccl_exchange(P, st);
       mk.end(9);
-      stage_near(P, mask, st, mk);
+      if (!overlap) stage_near(P, mask, st, mk);
     }
-    stage_down(P, mask, P->xc.recvbuf, st, mk, tr);
+    stage_down(P, mask, P->xc.recvbuf, st, mk, tr, overlap ? P->ev_near : nullptr);
     mk.begin(8);
     if (P->comm) nccl_allgather_out(P, st);
     fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
@@ -1527,8 +1548,8 @@ fda_status fda_apply_up(fda_plan P, const double* phi, double* sendbuf) {
   try {
     Marks mk;
     Trace tr;
-    stage_up(P, FDA_PHASE_ALL, reinterpret_cast<const double2*>(phi), reinterpret_cast<double2*>(sendbuf), P->stream,
-             mk, tr);
+    stage_permute(P, reinterpret_cast<const double2*>(phi), P->stream, mk);
+    stage_up(P, FDA_PHASE_ALL, reinterpret_cast<double2*>(sendbuf), P->stream, mk, tr);
     ck(cudaGetLastError());
   } catch (const CudaFail& f) {
     P->sticky_error = true;
@@ -1682,6 +1703,9 @@ fda_status fda_plan_destroy(fda_plan P) {
   if (P->ev_up) cudaEventDestroy(P->ev_up);
   if (P->ev_x) cudaEventDestroy(P->ev_x);
   if (P->xstream) cudaStreamDestroy(P->xstream);
+  if (P->ev_perm) cudaEventDestroy(P->ev_perm);
+  if (P->ev_near) cudaEventDestroy(P->ev_near);
+  if (P->nstream) cudaStreamDestroy(P->nstream);
   free_plan(P);
   delete P;
   return FDA_OK;

@@ -712,6 +712,51 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       D.U = sv.U;
       D.V = sv.V;
       D.sig = sv.s;
+      // Verification on held-out samples (SURVEY.md §8(b) FDA_ERR_SETUP_ACCURACY): 48 random unit charges in
+      // the source cube, their field at 160 random points of this wedge's far target boxes, directly and
+      // through the directional expansion (check potentials at a -> R^+ -> equivalent densities at b).
+      {
+        std::mt19937_64 rng(977u + 131u * (uint64_t)rd + 7u * (uint64_t)l);
+        std::uniform_real_distribution<double> U1(-0.5, 0.5);
+        std::vector<std::array<int, 3>> offs;
+        for (int i = -span; i <= span; ++i)
+          for (int j = -span; j <= span; ++j)
+            for (int kk = -span; kk <= span; ++kk) {
+              const int dm = std::max({std::abs(i), std::abs(j), std::abs(kk)});
+              const double v[3] = {(double)i, (double)j, (double)kk};
+              if (dm > L.R && face_dir(v, m) == rd) offs.push_back({i, j, kk});
+            }
+        if (!offs.empty()) {
+          std::vector<P3> ys(48), ts(160);
+          std::vector<cplx> qy(ys.size());
+          for (size_t j = 0; j < ys.size(); ++j) {
+            ys[j] = {U1(rng) * L.w, U1(rng) * L.w, U1(rng) * L.w};
+            qy[j] = cplx(U1(rng), U1(rng));
+          }
+          for (auto& t : ts) {
+            const auto& o = offs[rng() % offs.size()];
+            t = {(o[0] + U1(rng)) * L.w, (o[1] + U1(rng)) * L.w, (o[2] + U1(rng)) * L.w};
+          }
+          const Mat Gay = Gmat(k, D.ap, ys), Gty = Gmat(k, ts, ys), Gtb = Gmat(k, ts, D.bp);
+          std::vector<cplx> c(D.ap.size(), 0.0), w_(D.sig.size(), 0.0), sg(D.bp.size(), 0.0);
+          for (size_t j = 0; j < ys.size(); ++j)
+            for (size_t i = 0; i < D.ap.size(); ++i) c[i] += Gay((int64_t)i, (int64_t)j) * qy[j];
+          for (size_t r = 0; r < D.sig.size(); ++r) {  // sigma = V S^-1 U^H c
+            for (size_t i = 0; i < D.ap.size(); ++i) w_[r] += std::conj(D.U((int64_t)i, (int64_t)r)) * c[i];
+            w_[r] /= D.sig[r];
+          }
+          for (size_t b = 0; b < D.bp.size(); ++b)
+            for (size_t r = 0; r < D.sig.size(); ++r) sg[b] += D.V((int64_t)b, (int64_t)r) * w_[r];
+          double num = 0, den = 0;
+          for (size_t t = 0; t < ts.size(); ++t) {
+            cplx ud = 0, ue = 0;
+            for (size_t j = 0; j < ys.size(); ++j) ud += Gty((int64_t)t, (int64_t)j) * qy[j];
+            for (size_t b = 0; b < D.bp.size(); ++b) ue += Gtb((int64_t)t, (int64_t)b) * sg[b];
+            num += std::norm(ue - ud), den += std::norm(ud);
+          }
+          D.verr = std::sqrt(num / std::max(den, 1e-300));
+        }
+      }
     }
     int smax = 0;
     for (auto& D : L.reps) smax = std::max(smax, (int)D.sig.size());
@@ -719,9 +764,16 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     if (opt.verbose) {
       log << "level " << l << " HF m=" << m << " reps=" << L.reps.size() << " s=" << smax << " ranks:";
       for (auto& D : L.reps) log << " " << D.bp.size() << "/" << D.sig.size();
-      log << "\n";
+      double vmax = 0;
+      for (auto& D : L.reps) vmax = std::max(vmax, D.verr);
+      log << " held-out error max " << vmax << "\n";
     }
   }
+
+  // the HF directional sets must reproduce held-out far fields to the requested accuracy
+  for (const Level& L : P.levels)
+    for (const DirRep& D : L.reps)
+      if (D.verr > std::max(eps, 20.0 * P.eps_int)) return "SETUP_ACCURACY";
 
   // point sets of a slot direction (relative to the cube centre)
   auto hf_b = [&](const Level& L, int d) {

@@ -67,6 +67,7 @@ struct DirRep {         // HF directional point sets of one orbit representative
   std::vector<std::array<double, 3>> bp, ap;
   Mat U, V;             // truncated SVD of R_up = G(a, b): U (na x s), V (nb x s)
   std::vector<double> sig;
+  double verr = 0;      // relative error of the expansion on held-out far-field samples (build_plan)
 };
 
 struct Level {

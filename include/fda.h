@@ -97,13 +97,16 @@ typedef struct {
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1);
                               nranks <= 64; see fda_plan_create_dist / fda_apply_up */
   int32_t verbose;         /* plan log (fda_plan_log) */
-  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 30 (R23) */
+  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
   int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
                               FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat);
                               FDA_KERNEL_T1: K = G + alpha dG/dn_y (eq_sum; Table 1 mode,
                               SURVEY §8(f) row 2: pass unit weights and no correction for the paper's summation) */
   int32_t host_only;       /* diagnostics: build the host plan only (tree, lists, operators), no device;
                               fda_apply* then returns FDA_ERR_STATE.  Lets CPU tests audit the lists. */
+  int32_t original;        /* 1: the paper's "original" FDA for Table 1: expansions are the
+                              equivalent densities (no SVD reduction of the basis), dense unreduced M2L, no low
+                              rank (R24); default 0 = the improved FDA */
 } fda_options;
 
 typedef struct {

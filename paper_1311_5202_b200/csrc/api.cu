@@ -591,12 +591,27 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
         const fda::Mat& V = L.hf ? L.reps[ri].V : L.lfV;
         const std::vector<double>& sg = L.hf ? L.reps[ri].sig : L.lfsig;
         const int sr = (int)sg.size();
-        std::vector<cplx> vt((size_t)sr * V.m), su((size_t)sr * U.m);
-        for (int64_t i = 0; i < V.m; ++i)
-          for (int r = 0; r < sr; ++r) vt[r + (size_t)i * sr] = V(i, r);
-        for (int64_t i = 0; i < U.m; ++i)
-          for (int r = 0; r < sr; ++r) su[r + (size_t)i * sr] = std::conj(U(i, r)) / sg[r];
-        fV[ri] = up_c(V.a), fVT[ri] = up_c(vt), fSU[ri] = up_c(su), fs[ri] = sr;
+        if (!L.orig) {
+          std::vector<cplx> vt((size_t)sr * V.m), su((size_t)sr * U.m);
+          for (int64_t i = 0; i < V.m; ++i)
+            for (int r = 0; r < sr; ++r) vt[r + (size_t)i * sr] = V(i, r);
+          for (int64_t i = 0; i < U.m; ++i)
+            for (int r = 0; r < sr; ++r) su[r + (size_t)i * sr] = std::conj(U(i, r)) / sg[r];
+          fV[ri] = up_c(V.a), fVT[ri] = up_c(vt), fSU[ri] = up_c(su), fs[ri] = sr;
+        } else {
+          // original mode (Table 1): the expansion is the equivalent density itself -- identity reduction,
+          // M2M left factor R^+ = V Sigma^-1 U^H (n_b x n_a)
+          const int nb_ = (int)V.m;
+          std::vector<cplx> id((size_t)nb_ * nb_, 0.0), rp((size_t)nb_ * U.m, 0.0);
+          for (int b = 0; b < nb_; ++b) id[b + (size_t)b * nb_] = 1.0;
+          for (int64_t i = 0; i < U.m; ++i)
+            for (int b = 0; b < nb_; ++b) {
+              cplx v = 0;
+              for (int r = 0; r < sr; ++r) v += V(b, r) * std::conj(U(i, r)) / sg[r];
+              rp[b + (size_t)i * nb_] = v;
+            }
+          fV[ri] = up_c(id), fVT[ri] = fV[ri], fSU[ri] = up_c(rp), fs[ri] = nb_;
+        }
       }
       for (int d = 0; d < nd; ++d) {
         if (L.hf && L.dir_rep[d] < 0) continue;
@@ -1092,10 +1107,12 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     if (o.hf_max_rows > 0) fo.hf_max_rows = o.hf_max_rows;
     if (o.hf_spacing > 0) fo.hf_spacing = o.hf_spacing;
     fo.verbose = o.verbose;
+    fo.original = o.original != 0;
+    if (fo.original) fo.lowrank = 0;  // the original FDA has no low-rank M2L
     // operators and HF directional sets on the device (plan_dev.cu); host-only plans (list audits) skip the
     // operators; FDA_HOST_OPS=1 builds them on the host (linalg.cpp) instead, for cross-checks
     const bool host_ops = getenv("FDA_HOST_OPS") && getenv("FDA_HOST_OPS")[0] == '1';
-    fo.dev_ops = o.host_only || !host_ops;
+    fo.dev_ops = o.host_only || !host_ops || fo.original;
     if (!o.host_only && !host_ops) fo.select = dev_select;
     std::string err;
     fda::TreeIn tin;

@@ -183,7 +183,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   // DESIGN.md R11 / R23: expansion truncation (R+, HF interpolative selection) at eps_int, low-rank M2L
   // truncation at eps_lr (measured: the low-rank cut contributes no visible error at eps_int)
   P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
-  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 30.0;
+  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 3.0;
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
   P.np = leaf_size_for(eps, opt.np);
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;
@@ -581,7 +581,10 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     L.lfU = sv.U;
     L.lfV = sv.V;
     L.lfsig = sv.s;
-    L.s = (int)sv.s.size();
+    // the "original" FDA (Table 1) keeps the expansions as equivalent densities on all
+    // nsurf points (no SVD reduction of the basis, R24)
+    L.s = opt.original ? L.nsurf : (int)sv.s.size();
+    L.orig = opt.original;
   }
 
   const double tlf = now();
@@ -761,6 +764,11 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     int smax = 0;
     for (auto& D : L.reps) smax = std::max(smax, (int)D.sig.size());
     L.s = smax;
+    if (opt.original) {  // original mode: expansions are the equivalent densities on the wedge's points
+      L.orig = true;
+      L.s = 0;
+      for (auto& D : L.reps) L.s = std::max(L.s, (int)D.bp.size());
+    }
     if (opt.verbose) {
       log << "level " << l << " HF m=" << m << " reps=" << L.reps.size() << " s=" << smax << " ranks:";
       for (auto& D : L.reps) log << " " << D.bp.size() << "/" << D.sig.size();
@@ -920,6 +928,9 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
         for (double v : sv.s)
           if (v >= P.eps_lr * sv.s[0]) ++r;
         if (2 * r < std::max(Kt.m, Kt.n)) {
+          // rounded up to the kernel's tile height of 8 (free accuracy, R23)
+          const int r8 = std::min<int>((r + 7) / 8 * 8, (int)sv.s.size());
+          if (2 * r8 < std::max(Kt.m, Kt.n)) r = r8;
           rank = r;
           // U^ = Q U_R S (s x r), V^ = V_R^H (r x s), padded to the level size
           Mat QU = gemm(Q, 'N', sv.U, 'N');
@@ -988,11 +999,23 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     const int s = L.s, ns = L.nsurf;
     O.S.assign((size_t)s * ns, cplx(0));
     O.T.assign((size_t)ns * s, cplx(0));
-    for (int r = 0; r < s; ++r)
-      for (int i = 0; i < ns; ++i) {
-        O.S[r + (size_t)i * s] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // Sigma^-1 U^H
-        O.T[i + (size_t)r * ns] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // conj(U) Sigma^-1
-      }
+    if (!L.orig) {
+      for (int r = 0; r < s; ++r)
+        for (int i = 0; i < ns; ++i) {
+          O.S[r + (size_t)i * s] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // Sigma^-1 U^H
+          O.T[i + (size_t)r * ns] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // conj(U) Sigma^-1
+        }
+    } else {
+      // original mode: equivalent densities R^+ c = V Sigma^-1 U^H c (S2M) and its transpose (L2T)
+      const int sr = (int)L.lfsig.size();
+      for (int b = 0; b < s; ++b)
+        for (int i = 0; i < ns; ++i) {
+          cplx v = 0;
+          for (int r = 0; r < sr; ++r) v += L.lfV(b, r) * std::conj(L.lfU(i, r)) / L.lfsig[r];
+          O.S[b + (size_t)i * s] = v;
+          O.T[i + (size_t)b * ns] = v;
+        }
+    }
     P.leafops.push_back(std::move(O));
   }
   P.t_ops = now() - t0;

@@ -24,7 +24,7 @@ namespace fda {
 struct Options {
   int np = 0;               // leaf threshold N_p; 0 -> from eps (eq_npleaf, sign-corrected)
   double eps_int = 0;       // expansion truncation tolerance; 0 -> eps / 100 (R11)
-  double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps / 30 (R23)
+  double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps / 3 (R23)
   int lf_p_low = 0;         // LF surface points per edge for w/lambda < lf_p_switch; 0 -> 6 + dp(eps)
   int lf_p_high = 0;        // ... for w/lambda >= lf_p_switch; 0 -> 8 + dp(eps)  (R17)
   double lf_p_switch = 0.75;
@@ -37,6 +37,9 @@ struct Options {
   // Translation operators (M2M / L2L / M2L matrices) built on the device (plan_dev.cu) after the host plan:
   // build_plan then only records which operators are needed (Trans::need, M2LGroup with rank = -2).
   bool dev_ops = false;
+  // The paper's "original" FDA (Table 1): no SVD reduction of the expansion basis, dense unreduced M2L
+  // (requires dev_ops; low rank off)
+  bool original = false;
   // Pivoted column selection on A[i, j] = G(X_i - Y_j) rs_i cs_j (empty rs / cs: 1) with tolerance tol relative
   // to the largest column, at most maxrank pivots (R16).  Empty: the host pivoted QR (linalg.cpp).
   std::function<std::vector<int64_t>(const std::vector<std::array<double, 3>>& X,
@@ -93,8 +96,12 @@ struct Level {
   std::vector<int> dir_rep;      // dir -> index into reps
   std::vector<Sym> dir_sym;      // dir -> g with P_dir = g P_rep
   std::vector<DirRep> reps;
+  bool orig = false;  // original (unreduced) mode: expansions are equivalent densities (Options::original)
   // the expansion length of direction d (HF wedges are truncated separately; s is their maximum)
-  int sdir(int d) const { return hf && !reps.empty() ? (int)reps[dir_rep[d]].sig.size() : s; }
+  int sdir(int d) const {
+    if (!hf || reps.empty()) return s;
+    return orig ? (int)reps[dir_rep[d]].bp.size() : (int)reps[dir_rep[d]].sig.size();
+  }
 };
 
 struct HostPlan {

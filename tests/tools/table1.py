@@ -4,11 +4,14 @@
 
 For each Table-1 point set (cube-sphere, N = 73,728 * 4^j, k = 8 pi 2^j, ~20 points per wavelength)
 and each eps: the summation p_i = sum_{j != i} [G + alpha dG/dn_y] q_j (eq_sum, alpha = i/k, random
-q with mean 0, unit weights) by the FDA apply in "improved" mode (reduced + low-rank M2L, the
-default) and with the low-rank step off (lowrank = 0: reduced dense K~; our reduction is not
-optional, so this is not the paper's "original"); eps_a at N_t = 200 random targets against the
-oracle's direct sum.  Prints one JSON line per (row, mode); times are CUDA-event
-phase times of one apply on this B200 (the paper's are single-core CPU seconds: context only).
+q with mean 0, unit weights) by the FDA apply in the paper's three settings: "original" (unreduced
+equivalent-density expansions, dense M2L: fda_options.original = 1, R24), "reduced" (SVD-
+reduced basis, dense K~: lowrank = 0) and "improved" (reduced + low-rank M2L, the default); eps_a at
+N_t = 200 random targets against the oracle's direct sum and the device memory of the
+plan (Table 1's M column).  One JSON line per (row, eps, mode); times are CUDA-event phase times of one
+apply on this B200 (the paper's are single-core CPU seconds: context only).
+
+    python tests/tools/table1.py [--rows t1,t1b,...] eps ...
 """
 import json
 import os
@@ -27,9 +30,16 @@ ROWS = [("t1", 32, 8 * np.pi), ("t1b", 64, 16 * np.pi), ("t1c", 128, 32 * np.pi)
 
 
 def main():
-    eps_list = [float(a) for a in sys.argv[1:]] or [1e-4]
+    args = sys.argv[1:]
+    rows_sel = None
+    if args and args[0] == "--rows":
+        rows_sel = set(args[1].split(","))
+        args = args[2:]
+    eps_list = [float(a) for a in args] or [1e-4]
     dev = torch.device("cuda", 0)
     for name, m, k in ROWS:
+        if rows_sel and name not in rows_sel:
+            continue
         x, n, w, hmax, smp = synth.quadrature_cloud(synth.cube_sphere(m))
         N = x.shape[0]
         ones = np.ones(N)
@@ -40,12 +50,17 @@ def main():
         d_q = torch.from_numpy(q.view(np.float64).copy()).to(dev)
         d_p = torch.empty_like(d_q)
         for eps in eps_list:
-            for mode, lowrank in (("improved", 1), ("no-lowrank", 0)):
+            for mode, lowrank, orig in (("original", 0, 1), ("reduced", 0, 0), ("improved", 1, 0)):
                 t0 = time.time()
+                torch.cuda.synchronize()
+                mem0 = torch.cuda.mem_get_info()[0]
                 h = fda.fda_plan_create(torch.from_numpy(x).to(dev), torch.from_numpy(n).to(dev),
                                         torch.from_numpy(ones).to(dev), k, alpha, eps,
-                                        fda.fda_options_default(kernel=fda.FDA_KERNEL_T1, lowrank=lowrank))
+                                        fda.fda_options_default(kernel=fda.FDA_KERNEL_T1, lowrank=lowrank,
+                                                                original=orig))
                 t_plan = time.time() - t0
+                torch.cuda.synchronize()
+                plan_mem = (mem0 - torch.cuda.mem_get_info()[0]) / 1e9
                 fda.fda_apply(h, d_q, d_p)
                 ph = None
                 for _ in range(3):
@@ -56,7 +71,8 @@ def main():
                 print(json.dumps({"row": name, "N": N, "k": k, "eps": eps, "mode": mode,
                                   "eps_a": oracle.rel_l2(got[rows], ref), "apply_ms": sum(ph.values()),
                                   "m2l_ms": ph["m2l"], "up_ms": ph["s2m"] + ph["m2m"], "plan_s": round(t_plan, 1),
-                                  "device_gb": st["device_bytes"] / 1e9, "m2l_gflop": st["flops_m2l"] / 1e9}),
+                                  "device_gb": st["device_bytes"] / 1e9, "m2l_gflop": st["flops_m2l"] / 1e9,
+                                  "plan_mem_gb": plan_mem}),
                       flush=True)
 
 

@@ -475,16 +475,28 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
         }
       }
     }
-    std::vector<int32_t> keys;
+    // merge the threads' buckets per offset key (ascending key order) and sort each by target, in parallel
+    std::vector<size_t> keys;
     for (size_t key = 0; key < buckets.size(); ++key) {
       size_t tot = 0;
       for (int t = 0; t < nth; ++t) tot += tb[t][key].size();
-      if (!tot) continue;
-      std::vector<PairL> v;
+      if (tot) keys.push_back(key);
+    }
+    lv_pairs[l].resize(keys.size());
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t q = 0; q < (int64_t)keys.size(); ++q) {
+      const size_t key = keys[q];
+      std::vector<PairL>& v = lv_pairs[l][q];
+      size_t tot = 0;
+      for (int t = 0; t < nth; ++t) tot += tb[t][key].size();
       v.reserve(tot);
-      for (int t = 0; t < nth; ++t) v.insert(v.end(), tb[t][key].begin(), tb[t][key].end());
-      std::sort(v.begin(), v.end(), [](const PairL& a, const PairL& b) { return a.b < b.b; });
-      lv_pairs[l].push_back(std::move(v));
+      for (int t = 0; t < nth; ++t) {
+        v.insert(v.end(), tb[t][key].begin(), tb[t][key].end());
+        std::vector<PairL>().swap(tb[t][key]);
+      }
+      std::stable_sort(v.begin(), v.end(), [](const PairL& a, const PairL& b) { return a.b < b.b; });
+    }
+    for (size_t key : keys) {
       const int kk = (int)key;
       lv_offs[l].push_back({kk / (D * D) - span, (kk / D) % D - span, kk % D - span});
     }
@@ -503,22 +515,19 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     L.in_slot.assign(nc * L.ndir, -1);
     grp_dir[l].assign(lv_offs[l].size(), 0);
     if (lmin < 0 || l < lmin) continue;
-    auto add_out = [&](int64_t c, int d) {
-      int64_t& s = L.out_slot[c * L.ndir + d];
-      if (s < 0) s = 1;
-    };
-    auto add_in = [&](int64_t c, int d) {
-      int64_t& s = L.in_slot[c * L.ndir + d];
-      if (s < 0) s = 1;
-    };
+    // slot marks (idempotent stores of 1: relaxed atomics, so the pair loop can run in parallel)
+    auto add_out = [&](int64_t c, int d) { __atomic_store_n(&L.out_slot[c * L.ndir + d], (int64_t)1, __ATOMIC_RELAXED); };
+    auto add_in = [&](int64_t c, int d) { __atomic_store_n(&L.in_slot[c * L.ndir + d], (int64_t)1, __ATOMIC_RELAXED); };
     if (!L.hf) {
       for (int64_t c = 0; c < nc; ++c) add_out(c, 0), add_in(c, 0);
     } else {
       for (size_t g = 0; g < lv_offs[l].size(); ++g) {
         const double v[3] = {(double)lv_offs[l][g][0], (double)lv_offs[l][g][1], (double)lv_offs[l][g][2]};
-        const int d = face_dir(v, L.m);  // source -> target direction
-        grp_dir[l][g] = d;
-        const int t = anti_dir(d, L.m);
+        grp_dir[l][g] = face_dir(v, L.m);  // source -> target direction
+      }
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int64_t g = 0; g < (int64_t)lv_offs[l].size(); ++g) {
+        const int d = grp_dir[l][g], t = anti_dir(d, L.m);
         for (const PairL& pr : lv_pairs[l][g]) add_out(pr.c, d), add_in(pr.b, t);
       }
       if (l - 1 >= lmin && P.levels[l - 1].hf) {  // closure from parent slots
@@ -900,6 +909,12 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   const double tm2m = now();
   // ---- M2L groups: K~ = U_dn^H K V_up = V^T G(delta + b_tgt, b_src) V   (eq_cmpk), low rank (eq_lrdk)
   P.m2l_pool.assign(nlev, {});
+  {
+    size_t tot = 0;
+    for (int l = 0; l < nlev; ++l)
+      for (const auto& v : lv_pairs[l]) tot += v.size();
+    P.m2l_tgt.reserve(tot), P.m2l_src.reserve(tot);
+  }
   for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
     Level& L = P.levels[l];
     const int s = L.s;

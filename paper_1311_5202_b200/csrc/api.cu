@@ -21,12 +21,13 @@
 using fda::cplx;
 
 // FP64 flops per kernel evaluation (P2P point pair; S2M / L2T surface evaluation) by operator kind
-// (BM_H, BM_G, T1): (2 x DFMA + DADD + DMUL) thread instructions per evaluation of k_p2p / k_s2m_check /
-// k_l2t_eval, counted by ncu (profiles/r02_fp64_counts.md); they turn the evaluation counts into the
-// algorithmic flops the roofline fractions of the ALU phases use.
-static const double FLOP_P2P[3] = {100.0, 60.0, 60.0};
-static const double FLOP_S2M[3] = {40.0, 30.0, 60.0};
-static const double FLOP_L2T = 60.0;
+// (BM_H, BM_G, T1): (2 x DFMA + DADD + DMUL) thread instructions per evaluation, counted by ncu
+// (smsp__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on.sum) over k_p2p / k_s2m_check / k_l2t_eval
+// of a config-3 apply divided by the plan's evaluation counts (profiles/r02/ncu_alu_counts_c3.csv):
+// BM_H P2P 109.8, S2M (dipole) 77.1, L2T 86.1.  The BM_G / T1 entries are estimates (not measured).
+static const double FLOP_P2P[3] = {109.8, 75.0, 75.0};
+static const double FLOP_S2M[3] = {77.1, 60.0, 86.1};
+static const double FLOP_L2T = 86.1;
 
 namespace {
 
@@ -282,6 +283,8 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     for (int64_t p = 0; p < np; ++p) dix.emplace(out_dir[G.out[p]], (int64_t)dix.size());
     const int64_t nd = (int64_t)dix.size();
     S = std::max<int64_t>((int64_t)(ppg / (2 * cols)), (8 * 148 + nd - 1) / nd);
+    // FDA_GT_SLABS=n: n Morton slabs per output direction (experiments)
+    if (getenv("FDA_GT_SLABS")) S = std::max(1, atoi(getenv("FDA_GT_SLABS")) / (int)std::max<int64_t>(1, nd));
     S = std::max<int64_t>(1, std::min<int64_t>({S, 4096, ncubes}));
   }
   if (!force_owned && (!use_auto || ppg / (double)S < 0.75 * cols)) {
@@ -690,7 +693,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       J.n_items = ng;
       J.a = upload(P, ia), J.b = upload(P, ib), J.shift = upload(P, sh);
       J.sets = d_sets, J.k = H.k, J.s_out = L.s, J.s_in = L.s;
-      J.compress = H.opt.lowrank ? 1 : 0, J.eps_lr = H.eps_lr;
+      J.compress = H.opt.lowrank ? 1 : 0, J.eps_lr = H.eps_lr_level(L);
       set_max(bset[l], &J.maxn);
       J.maxs = L.s;
       std::vector<int32_t> rk(ng, -1);

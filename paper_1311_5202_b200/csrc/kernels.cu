@@ -399,6 +399,9 @@ __device__ __forceinline__ void bulk_issue_cols(double2* Y, const double2* Ys, c
   bulk_commit();
 }
 
+// sector-complete reductions in the atomic epilogue (kernels.cu gt_stage; FDA_GT_SECTOR=1 enables them)
+__constant__ int gt_sector_red = 0;
+
 __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 + 4; }  // >= k, = 4 mod 8
 
 // One GEMM stage: C (Mt*8 x GT_P) = A (Mt*8 x Kt*4, fragment order) x B (Kt*4 x GT_P, smem double2).
@@ -450,6 +453,35 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
         dmma(acc[c][1][0], acc[c][1][1], ai, b.y);
         dmma(acc[c][2][0], acc[c][2][1], as, b.x + b.y);
       }
+    }
+    if (MODE == 2 && gt_sector_red && !(s_out & 1)) {
+      // Sector-complete FP64 reductions.  The L2 applies REDs per 32-byte sector; a lane's own values
+      // (real / imaginary part of one row for two columns) cover half of a sector per instruction.  The
+      // values are redistributed by shuffles so that in each of the 4 instructions per column tile the 4
+      // lanes 4q..4q+3 add (re, im) of rows 2h and 2h+1 of one column -- one full, 32-byte aligned sector
+      // (s_out even: every Y row pair starts on a sector).  Halves the L2 sector operations.
+#pragma unroll
+      for (int c = 0; c < GT_CT; ++c) {
+        double rr[2], mm[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          rr[i] = acc[c][0][i] - acc[c][1][i];
+          mm[i] = acc[c][2][i] - acc[c][0][i] - acc[c][1][i];
+        }
+        const int q = lane >> 2, e = lane & 3, tt = q & 3;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = j >> 1, h = 2 * (j & 1) + (q >> 2);
+          const int r = 2 * h + (e >> 1), src = r * 4 + tt;
+          const double vre = __shfl_sync(0xffffffffu, rr[i], src);
+          const double vim = __shfl_sync(0xffffffffu, mm[i], src);
+          const double v = (e & 1) ? vim : vre;
+          const int col = (cg * GT_CT + c) * 8 + 2 * tt + i, rw = mt * 8 + r;
+          if (rw < s_out && col < nb && v != 0.0)
+            atomicAdd(reinterpret_cast<double*>(Y + (int64_t)sOut[col] * s_out + rw) + (e & 1), v);
+        }
+      }
+      continue;
     }
 #pragma unroll
     for (int c = 0; c < GT_CT; ++c)
@@ -932,6 +964,15 @@ static cudaError_t gt_launch_ws(const GTrans& T, const double2* X, double2* Y, s
 
 cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return cudaSuccess;
+  static const bool sector_on = [] {
+    const bool on = getenv("FDA_GT_SECTOR") && getenv("FDA_GT_SECTOR")[0] == '1';
+    if (on) {
+      const int one = 1;
+      cudaMemcpyToSymbol(gt_sector_red, &one, sizeof(int));
+    }
+    return on;
+  }();
+  (void)sector_on;
   // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
   static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
   if (ws_ok && T.atomic && T.all_lowrank) {

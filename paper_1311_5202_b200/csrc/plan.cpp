@@ -593,6 +593,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     // the "original" FDA (Table 1) keeps the expansions as equivalent densities on all
     // nsurf points (no SVD reduction of the basis, R24)
     L.s = opt.original ? L.nsurf : (int)sv.s.size();
+    L.s += L.s & 1;  // even: every Y row pair is sector-aligned (kernels.cu sector-complete reductions)
     L.orig = opt.original;
   }
 
@@ -778,6 +779,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       L.s = 0;
       for (auto& D : L.reps) L.s = std::max(L.s, (int)D.bp.size());
     }
+    L.s += L.s & 1;  // even (sector-aligned Y row pairs)
     if (opt.verbose) {
       log << "level " << l << " HF m=" << m << " reps=" << L.reps.size() << " s=" << smax << " ranks:";
       for (auto& D : L.reps) log << " " << D.bp.size() << "/" << D.sig.size();
@@ -937,11 +939,12 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       std::vector<cplx>& out = gm[g];
       if (opt.lowrank && Kt.m > 1) {
         Mat Q, Rq;
-        std::vector<int64_t> piv = pivoted_qr(Kt, 0.1 * P.eps_lr, Kt.n, &Q, &Rq);
+        const double elr = P.eps_lr_level(L);
+        std::vector<int64_t> piv = pivoted_qr(Kt, 0.1 * elr, Kt.n, &Q, &Rq);
         SVD sv = svd_truncated(Rq, 0.0);
         int r = 0;
         for (double v : sv.s)
-          if (v >= P.eps_lr * sv.s[0]) ++r;
+          if (v >= elr * sv.s[0]) ++r;
         if (2 * r < std::max(Kt.m, Kt.n)) {
           // rounded up to the kernel's tile height of 8 (free accuracy, R23)
           const int r8 = std::min<int>((r + 7) / 8 * 8, (int)sv.s.size());
@@ -1015,7 +1018,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     O.S.assign((size_t)s * ns, cplx(0));
     O.T.assign((size_t)ns * s, cplx(0));
     if (!L.orig) {
-      for (int r = 0; r < s; ++r)
+      for (int r = 0; r < (int)L.lfsig.size(); ++r)
         for (int i = 0; i < ns; ++i) {
           O.S[r + (size_t)i * s] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // Sigma^-1 U^H
           O.T[i + (size_t)r * ns] = std::conj(L.lfU(i, r)) / L.lfsig[r];  // conj(U) Sigma^-1
@@ -1023,7 +1026,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     } else {
       // original mode: equivalent densities R^+ c = V Sigma^-1 U^H c (S2M) and its transpose (L2T)
       const int sr = (int)L.lfsig.size();
-      for (int b = 0; b < s; ++b)
+      for (int b = 0; b < std::min(s, ns); ++b)
         for (int i = 0; i < ns; ++i) {
           cplx v = 0;
           for (int r = 0; r < sr; ++r) v += L.lfV(b, r) * std::conj(L.lfU(i, r)) / L.lfsig[r];

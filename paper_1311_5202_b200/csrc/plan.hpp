@@ -157,6 +157,13 @@ struct HostPlan {
     std::vector<cplx> T;   // nsurf x s column-major  (conj(U) Sigma^-1)
   };
   std::vector<LeafOps> leafops;
+  // low-rank M2L truncation of a level (R23): eps_lr, tightened 10x on the low-frequency LF levels
+  // (w < lambda / 4), whose far fields of mean-zero densities cancel most (measured: kD = 1 far-field error
+  // 2.1e-3 at eps / 3, 5.8e-4 at eps / 30, profiles/r02)
+  double eps_lr_level(const Level& L) const {
+    const bool lowf = !L.hf && (k <= 0 || L.w * k / (2.0 * 3.14159265358979323846) < 0.25);
+    return lowf && opt.eps_lr <= 0 ? eps_lr / 10.0 : eps_lr;
+  }
   // stats
   double t_tree = 0, t_lists = 0, t_ops = 0;
   std::string log;

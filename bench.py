@@ -146,6 +146,8 @@ def main():
     ap.add_argument("--check-rows", type=int, default=2000)
     ap.add_argument("--ref-rows", type=int, default=200)
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the library's NCCL data plane (fda_plan_create_dist) even on one rank (tests the path)")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -162,7 +164,10 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        for key_, v_ in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(key_, v_)
         dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
     p, csr, phi = make_inputs(args.config)
@@ -171,7 +176,7 @@ def main():
     kernel = fda.FDA_KERNEL_BMG if args.kernel == "bmg" else fda.FDA_KERNEL_BMH
     opt = fda.fda_options_default(verbose=1 if args.verbose else 0, kernel=kernel)
     pts, nrm, wts = (torch.from_numpy(a).to(dev) for a in (p.x, p.n, p.w))
-    if world > 1:
+    if use_dist:
         # the library's own data plane: NCCL communicator inside libfda, partial-expansion
         # exchange + output all-gather inside fda_apply; the process group only distributes the NCCL id
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -274,7 +279,9 @@ def main():
              "s2m": st["flops_s2m"], "l2t": st["flops_l2t"]}
     dom = max(per, key=lambda k_: per[k_]) if per else "m2l"
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02", "traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"config{args.config}", {}).get(dom)
@@ -322,7 +329,7 @@ def main():
         line["gpu_launches"] = launches_step * args.steps
         print(json.dumps(line), flush=True)
     fda.fda_plan_destroy(h)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

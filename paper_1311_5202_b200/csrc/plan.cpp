@@ -593,7 +593,6 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     // the "original" FDA (Table 1) keeps the expansions as equivalent densities on all
     // nsurf points (no SVD reduction of the basis, R24)
     L.s = opt.original ? L.nsurf : (int)sv.s.size();
-    L.s += L.s & 1;  // even: every Y row pair is sector-aligned (kernels.cu sector-complete reductions)
     L.orig = opt.original;
   }
 
@@ -779,7 +778,6 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
       L.s = 0;
       for (auto& D : L.reps) L.s = std::max(L.s, (int)D.bp.size());
     }
-    L.s += L.s & 1;  // even (sector-aligned Y row pairs)
     if (opt.verbose) {
       log << "level " << l << " HF m=" << m << " reps=" << L.reps.size() << " s=" << smax << " ranks:";
       for (auto& D : L.reps) log << " " << D.bp.size() << "/" << D.sig.size();

@@ -1,10 +1,12 @@
-"""profiles/traffic.json from an ncu metric capture of one apply (tools/job_*.sh mem_*.csv):
-DRAM bytes (read + write) per apply, summed over the launches of each phase, in launch order of
-api.cu's apply: permute, p2p, csr, s2m (check + product per LF level), m2m (per transition),
-m2l (per level), l2l (per transition), l2t (product + evaluation per LF level), unpermute.
+"""profiles/r02/traffic.json from an ncu launch list of the bench command (tools/jobs/r02_ncu.sh,
+`-k regex:"k_(gtrans|p2p|csr|s2m|l2t|permute|unpermute|xpack|xunpack)"`, metrics gpu__time_duration.sum and
+dram__bytes_{read,write}.sum): DRAM bytes (read + write) per apply, summed over the launches of each
+phase of the second apply in the list.  Launch order of api.cu's apply: permute, p2p, csr, then per LF
+leaf level (S2M check + product), the M2M transitions, the M2L launches (one or two per level), the
+L2L transitions, per LF leaf level (L2T product + evaluation), unpermute.
 
-    python tools/make_traffic.py gpurun_out/mem_c5v11.csv config5 NLF NTRANS NM2L
-(NLF LF leaf levels, NTRANS transitions, NM2L M2L levels of the plan; config 5: 2 4 5)
+    python tools/make_traffic.py gpurun_out/launches_c5.csv config5 NLF NTRANS [out.json]
+(NLF: LF leaf levels of the plan, NTRANS: transitions; config 5: 2 5)
 """
 import csv
 import json
@@ -13,39 +15,44 @@ import sys
 
 
 def main():
-    path, key, nlf, ntr, nm2l = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+    path, key, nlf, ntr = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
+    out = sys.argv[5] if len(sys.argv) > 5 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                                "profiles", "r02", "traffic.json")
     rows = list(csv.reader(open(path)))
     hdr = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hdr]
-    per = {}
-    order = []
+    per, order = {}, []
     for r in rows[hdr + 1:]:
+        if len(r) != len(h):
+            continue
         i = int(r[h.index("ID")])
         if i not in per:
             order.append(i)
             per[i] = {"name": r[h.index("Kernel Name")]}
         per[i][r[h.index("Metric Name")]] = float(r[h.index("Metric Value")])
-    # find the start of an apply: k_permute_scale
-    start = next(j for j, i in enumerate(order) if per[i]["name"].startswith("k_permute_scale"))
+    starts = [j for j, i in enumerate(order) if "k_permute_scale" in per[i]["name"]]
+    a, b = starts[1], (starts[2] if len(starts) > 2 else len(order))
+    ids = order[a:b]
+    nm2l = len(ids) - 4 - 4 * nlf - 2 * ntr
     seq = ["permute", "p2p", "csr"] + ["s2m"] * (2 * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
           ["l2t"] * (2 * nlf) + ["unpermute"]
-    out = {}
-    # consecutive applies launch the same sequence: read it cyclically from the first k_permute_scale
-    # (the capture must hold at least one apply's worth of launches)
-    n = len(seq)
-    assert len(order) >= n, "capture shorter than one apply"
-    base = [order[start + j] if start + j < len(order) else order[start + j - n] for j in range(n)]
-    for ph, i in zip(seq, base):
+    assert len(seq) == len(ids), (len(seq), len(ids))
+    res = {}
+    for ph, i in zip(seq, ids):
         d = per[i]
-        b = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
-        out[ph] = out.get(ph, 0.0) + b
-    tp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
-    allt = json.load(open(tp)) if os.path.exists(tp) else {}
-    allt[key] = {k: int(v) for k, v in out.items()}
-    allt["_about"] = ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per apply and phase, summed over the "
-                      "phase's launches, from ncu metric captures (tools/make_traffic.py)")
-    json.dump(allt, open(tp, "w"), indent=1)
-    print(json.dumps(allt[key]))
+        res.setdefault(ph, {"dram_bytes": 0.0, "ms": 0.0, "launches": 0})
+        res[ph]["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+        res[ph]["ms"] += d.get("gpu__time_duration.sum", 0) / 1e6
+        res[ph]["launches"] += 1
+    tot = sum(v["ms"] for v in res.values())
+    for v in res.values():
+        v["share"] = v["ms"] / tot
+    data = json.load(open(out)) if os.path.exists(out) else {}
+    data[key] = {ph: v["dram_bytes"] for ph, v in res.items()}
+    data[key + "_detail"] = res
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump(data, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":

@@ -31,7 +31,7 @@ WORKLOADS = {
     "1": "unit sphere N=3072 kD=10 (configs[0])",
     "2": "sphere D=2 N=196608 kD=1 (configs[1])",
     "3": "sphere D=2 N=397488 kD=100 (configs[2])",
-    "4": "prolate spheroid 10:1:1 N~1M kD=400 (configs[3])",
+    "4": "prolate spheroid 10:1:1 N=999600 kD=400 (configs[3])",
     "5": "sphere D=2 N=4009008 kD=1000 eps=1e-4 (configs[4], the metric's workload)",
 }
 
@@ -312,7 +312,7 @@ def main():
                 "config": {"workload": WORKLOADS.get(args.config, args.config), "operator": args.kernel.upper(),
                            "parallelism": "single GPU" if world == 1 else
                            f"{world} Morton leaf ranges, NCCL partial-expansion exchange + output all-gather",
-                           "N": N, "k": p.k, "kD": 2 * p.k,
+                           "N": N, "k": p.k, "kD": p.k * float(np.ptp(p.x, axis=0).max()),
                            "eps": p.eps, "alpha": "i/k", "csr_nnz": int(st["csr_nnz"]),
                            "l2": "inputs larger than L2 (correction CSR %.1f GB)" % (st["csr_nnz"] * 20 / 1e9)},
                 "e2e": {"value": N / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(N * 16),

@@ -720,8 +720,10 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans(GTrans T, const double2* __r
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
-template <int GT_P, bool STAGE, bool YB>
-__global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* __restrict__ X,
+// NT threads: 256 (two CTAs per SM) or 512 (one CTA per SM: 227 KB of shared memory, so the LF levels'
+// operators can be staged too; 8 + 8 warps)
+template <int GT_P, bool STAGE, bool YB, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_gtrans_ws(GTrans T, const double2* __restrict__ X,
                                                       double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
   const int s_in = T.s_in, s_out = T.s_out;
@@ -734,11 +736,11 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   double* Ms = reinterpret_cast<double*>(Ys + (YB ? GT_P * s_out : 0));
   __shared__ int sOut[3][GT_P], sIn[3][GT_P];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool grpA = warp < GT_W / 2;  // stage-1 warps (and the gather); the rest run stage 2
+  const bool grpA = warp < (NT / 64);  // stage-1 warps (and the gather); the rest run stage 2
   const int64_t item = T.item_order[blockIdx.x];
   const int64_t e_beg = T.item_ptr[item], e_end = T.item_ptr[item + 1];
   if (e_beg >= e_end) return;
-  for (int i = tid; i < GT_P * ldx; i += GT_T) Xs[i] = make_double2(0.0, 0.0);
+  for (int i = tid; i < GT_P * ldx; i += NT) Xs[i] = make_double2(0.0, 0.0);
   // chunk list of the item: entries (groups) e, pairs [c, c + GT_P)
   auto advance = [&](int64_t& e, int64_t& c) {
     c += GT_P;
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
   const int kin_g = T.gsi ? (T.gsi[grp0] + 3) / 4 : kin, mout_g = T.gso ? (T.gso[grp0] + 7) / 8 : mout;
   const int xlen = min(4 * kin_g, s_in);
   auto issue_x = [&](int ib) {  // by the stage-1 warps
-    for (int c = warp; c < GT_P; c += GT_W / 2) {
+    for (int c = warp; c < GT_P; c += (NT / 64)) {
       const int src = sIn[ib][c];
       if (src < 0) continue;
       const double2* xs = X + (int64_t)src * s_in;
@@ -773,7 +775,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
     const int rank = T.grank[grp0], rt = (rank + 7) / 8;
     const double* src = T.pool + T.gmat[grp0];
     const int nd = (rt * kin + mout * 2 * rt) * 64;
-    for (int i = tid; i < nd / 2; i += GT_T) cp_async16(Ms + 2 * i, src + 2 * i);
+    for (int i = tid; i < nd / 2; i += NT) cp_async16(Ms + 2 * i, src + 2 * i);
     cp_async_commit();
   }
   int64_t ea = e_beg, ca = T.ig_pb[e_beg];  // chunk of the stage-1 warps (i)
@@ -794,10 +796,11 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const int rank = T.grank[grp], rt = (rank + 7) / 8;
       const double* Mg = STAGE ? Ms : T.pool + T.gmat[grp];
       cp_async_wait<0>();
-      named_bar(1, GT_T / 2);  // X of chunk i visible to the stage-1 warps
-      const int ct1 = (rt % 2 == 0 && GT_P >= 16) ? 2 : 1;  // units = rt x (GT_P / 8 / ct1)
+      named_bar(1, (NT / 2));  // X of chunk i visible to the stage-1 warps
+      // units = rt x (GT_P / 8 / ct1): a multiple of the NT / 64 stage-1 warps where possible
+      const int ct1 = (NT == 256 && rt % 2 == 0 && GT_P >= 16) ? 2 : 1;
       gt_stage_ct<GT_P, 0, STAGE>(ct1, Mg, rt, kin_g, 1, Xs, ldx, T0 + (i & 1) * GT_P * ldt, ldt, nullptr, nullptr, 0,
-                                  0, kin, 0, GT_W / 2);
+                                  0, kin, 0, (NT / 64));
     }
     (void)ia;
     if (!grpA && eb >= 0) {
@@ -810,17 +813,17 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
       const int kt2 = (rank + 3) / 4;
       const int nb = (int)min((int64_t)GT_P, T.ig_pe[eb] - cb);
       if (YB) {
-        if (ypend && warp == GT_W / 2) bulk_wait_read();  // Ys of the previous chunk read by the bulk engine
-        named_bar(2, GT_T / 2);
+        if (ypend && warp == (NT / 64)) bulk_wait_read();  // Ys of the previous chunk read by the bulk engine
+        named_bar(2, (NT / 2));
         gt_stage_ct<GT_P, 3, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt,
-                                    ldt, Ys, s_out, nullptr, nullptr, s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+                                    ldt, Ys, s_out, nullptr, nullptr, s_out, nb, 2 * rt, (NT / 64), (NT / 64));
         fence_async_smem();
-        named_bar(2, GT_T / 2);
-        if (warp == GT_W / 2) bulk_issue_cols(Y, Ys, sOut[ibb], s_out, nb, lane);
+        named_bar(2, (NT / 2));
+        if (warp == (NT / 64)) bulk_issue_cols(Y, Ys, sOut[ibb], s_out, nb, lane);
         ypend = true;
       } else {
         gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt,
-                                    ldt, nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, GT_W / 2, GT_W / 2);
+                                    ldt, nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, (NT / 64), (NT / 64));
       }
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
@@ -835,7 +838,7 @@ __global__ void __launch_bounds__(GT_T, 2) k_gtrans_ws(GTrans T, const double2* 
     }
     ++i;
   }
-  if (YB && warp == GT_W / 2) bulk_wait_all();
+  if (YB && warp == (NT / 64)) bulk_wait_all();
 }
 
 static size_t gt_smem_ws(const GTrans& T, int p, bool stage, bool yb) {
@@ -951,14 +954,14 @@ int gtrans_ws_rmax(int s_in) {
   return best;
 }
 
-template <int P, bool STG, bool YB>
+template <int P, bool STG, bool YB, int NT = 256>
 static cudaError_t gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_gtrans_ws<P, STG, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_gtrans_ws<P, STG, YB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_gtrans_ws<P, STG, YB><<<(unsigned)T.n_items, GT_T, sm, st>>>(T, X, Y);
+  k_gtrans_ws<P, STG, YB, NT><<<(unsigned)T.n_items, NT, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
 
@@ -982,6 +985,12 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
     // per SM; 32 columns with bulk outputs may take one CTA per SM with FDA_GT_WSP=32)
     static const int wsp = getenv("FDA_GT_WSP") ? atoi(getenv("FDA_GT_WSP")) : 0;
     const bool yb = gt_bulk();
+    // operators too large to stage next to two CTAs per SM (the LF levels): one 512-thread CTA per SM with
+    // the operator staged in shared memory (FDA_GT_WS512=0: off)
+    static const bool ws512 = !(getenv("FDA_GT_WS512") && getenv("FDA_GT_WS512")[0] == '0');
+    if (ws512 && !yb && !wsp && gt_smem_ws(T, 32, true, false) > budget &&
+        gt_smem_ws(T, 32, true, false) <= smem_optin())
+      return gt_launch_ws<32, true, false, 512>(T, X, Y, gt_smem_ws(T, 32, true, false), st);
     for (int p : {32, 16}) {
       if (wsp && p != wsp) continue;
       const size_t lim = wsp == p ? smem_optin() : budget;

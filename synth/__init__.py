@@ -372,7 +372,7 @@ CONFIGS = {
     "1c": ("sphere", 46, 200.0),
     "2": ("sphere", 64, 0.5),
     "3": ("sphere", 91, 50.0),
-    "4": ("spheroid", 0.0366, 20.0),
+    "4": ("spheroid", 0.0345, 20.0),
     "5": ("sphere", 289, 500.0),
     # Table-1 workloads: cube-sphere, ~20 points per wavelength, N = 73,728 * 4^j
     "t1": ("cubesphere", 32, 8 * np.pi),

@@ -238,7 +238,7 @@ int64_t frag_size(int rank, int s_out, int s_in) {
 // device pool dpool in fragment order (G.mat = offsets in doubles, plan_dev.cu).
 fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& out_cube,
                        const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, const cplx* raw,
-                       const double* dpool = nullptr) {
+                       const double* dpool = nullptr, const char* mode = nullptr) {
   fda::GTrans T;
   const int64_t ng = (int64_t)G.rank.size(), np = (int64_t)G.out.size();
   if (np == 0) return T;
@@ -266,7 +266,7 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   const int cols = fda::gtrans_cols(T);
   const double ppg = (double)np / (double)std::max<int64_t>(ng, 1);
   // FDA_GT_MODE=atomic|owned|auto forces the item kind (experiments); FDA_GT_CHUNK: pairs per atomic item
-  const char* gm = getenv("FDA_GT_MODE");
+  const char* gm = mode ? mode : getenv("FDA_GT_MODE");
   // Default: group-major items of <= 1024 pairs with atomic accumulation (measured at config 5: 400 ms
   // apply vs 440 ms with the automatic choice and 509 ms with owned items only; 1024 vs 256 pairs:
   // 332 vs 336 ms).
@@ -728,6 +728,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->st.flops_m2l += np * (G.rank[g] < 0 ? 8.0 * st_ * ss : 8.0 * G.rank[g] * (st_ + ss));
     }
     const cplx* raw = dev_ops ? nullptr : H.m2l_pool[l].data();
+    // FDA_M2L_MODE=owned|atomic: the item kind of the M2L launches only (experiments; FDA_GT_MODE: all)
+    const char* m2l_mode = getenv("FDA_M2L_MODE");
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
     // the nearest offsets) go to a second launch of the general kernel.
     const int rlim = fda::gtrans_ws_rmax(L.s);
@@ -760,10 +762,10 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       }
     }
     if (!G1.rank.empty() && !G2.rank.empty()) {
-      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
-      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
+      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
+      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
     } else {
-      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool);
+      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
     }
   }
   lap("m2l");

@@ -722,7 +722,10 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 // NT threads: 256 (two CTAs per SM) or 512 (one CTA per SM: 227 KB of shared memory, so the LF levels'
 // operators can be staged too; 8 + 8 warps)
-template <int GT_P, bool STAGE, bool YB, int NT>
+// OWN: owned items (T.atomic == 0: an item owns its output slots and walks several groups): plain
+// read-modify-write of Y instead of FP64 atomics; the operators are read from L2 (no staging) and the full
+// expansion lengths are used.
+template <int GT_P, bool STAGE, bool YB, int NT, bool OWN = false>
 __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_gtrans_ws(GTrans T, const double2* __restrict__ X,
                                                       double2* __restrict__ Y) {
   extern __shared__ double2 gsm2[];
@@ -760,7 +763,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_gtrans_ws(GTrans T, c
   // all groups of an atomic item are one group; stage its matrix once (all threads)
   const int grp0 = T.ig_group[e_beg];
   // the group's own expansion lengths (HF wedges shorter than the level's padded s; their tails are zero)
-  const int kin_g = T.gsi ? (T.gsi[grp0] + 3) / 4 : kin, mout_g = T.gso ? (T.gso[grp0] + 7) / 8 : mout;
+  const int kin_g = (T.gsi && !OWN) ? (T.gsi[grp0] + 3) / 4 : kin, mout_g = (T.gso && !OWN) ? (T.gso[grp0] + 7) / 8 : mout;
   const int xlen = min(4 * kin_g, s_in);
   auto issue_x = [&](int ib) {  // by the stage-1 warps
     for (int c = warp; c < GT_P; c += (NT / 64)) {
@@ -822,8 +825,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_gtrans_ws(GTrans T, c
         if (warp == (NT / 64)) bulk_issue_cols(Y, Ys, sOut[ibb], s_out, nb, lane);
         ypend = true;
       } else {
-        gt_stage_ct<GT_P, 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1, T0 + ((i + 1) & 1) * GT_P * ldt,
-                                    ldt, nullptr, 0, Y, sOut[ibb], s_out, nb, 2 * rt, (NT / 64), (NT / 64));
+        gt_stage_ct<GT_P, OWN ? 1 : 2, STAGE>(T.ct2 > 0 ? T.ct2 : GT_P / 8, U, mout_g, kt2, 1,
+                                              T0 + ((i + 1) & 1) * GT_P * ldt, ldt, nullptr, 0, Y, sOut[ibb], s_out,
+                                              nb, 2 * rt, (NT / 64), (NT / 64));
       }
     }
     __syncthreads();  // chunk i's T written, chunk i-1's outputs issued; X and index buffer ibb free
@@ -954,14 +958,14 @@ int gtrans_ws_rmax(int s_in) {
   return best;
 }
 
-template <int P, bool STG, bool YB, int NT = 256>
+template <int P, bool STG, bool YB, int NT = 256, bool OWN = false>
 static cudaError_t gt_launch_ws(const GTrans& T, const double2* X, double2* Y, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(k_gtrans_ws<P, STG, YB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_gtrans_ws<P, STG, YB, NT, OWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_gtrans_ws<P, STG, YB, NT><<<(unsigned)T.n_items, NT, sm, st>>>(T, X, Y);
+  k_gtrans_ws<P, STG, YB, NT, OWN><<<(unsigned)T.n_items, NT, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
 
@@ -978,6 +982,9 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
   (void)sector_on;
   // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
   static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
+  // owned low-rank items (FDA_GT_MODE=owned): the warp-specialised kernel with plain read-modify-write outputs
+  if (ws_ok && !T.atomic && T.all_lowrank && gt_smem_ws(T, 32, false, false) <= GT_SMEM_BUDGET)
+    return gt_launch_ws<32, false, false, 256, true>(T, X, Y, gt_smem_ws(T, 32, false, false), st);
   if (ws_ok && T.atomic && T.all_lowrank) {
     static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
                                                            : (size_t)GT_SMEM_BUDGET;

@@ -578,7 +578,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     const int dp = eps < 1e-4 ? (int)std::lround(std::log10(1e-4 / eps)) : 0;
     // explicit lf_p_low / lf_p_high options are used verbatim; the eps bump applies to the defaults only.
     // Default p: 6 for 0.25 <= w/lambda < 0.75, 7 below 0.25 (the low-frequency levels: measured far-field
-    // error 2.4e-3 with p = 6 against 5.8e-4 with p = 7 at kD = 1, profiles/r02_far_probe_c2.jsonl), 8 above.
+    // error 2.4e-3 with p = 6 against 5.8e-4 with p = 7 at kD = 1, profiles/r02/far_probe_c2.jsonl), 8 above.
     const int p_low = opt.lf_p_low > 0 ? opt.lf_p_low : (wl < 0.25 ? 7 : 6) + dp;
     const int p_high = opt.lf_p_high > 0 ? opt.lf_p_high : 8 + dp;
     L.p = wl < opt.lf_p_switch ? p_low : p_high;

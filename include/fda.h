@@ -92,7 +92,7 @@ typedef struct {
   double lf_p_switch;      /* w / lambda switch (default 0.75) */
   int32_t lowrank;         /* low-rank M2L when rank < s/2, default 1 */
   int32_t single_leaf;     /* debug: no far field, every pair P2P (default 0) */
-  int32_t hf_max_rows;     /* HF directional-set sample rows (default 6000) */
+  int32_t hf_max_rows;     /* HF directional-set sample rows; 0 (default): 6000 x (1 + decades of eps below 1e-4) */
   double hf_spacing;       /* HF candidate spacing in wavelengths (default 0.25) */
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1);
                               nranks <= 64; see fda_plan_create_dist / fda_apply_up */

@@ -1176,6 +1176,11 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
       free_plan(P.get());
       return s;
     }
+    {  // return the plan builder's stream-ordered scratch (cudaMallocAsync pool) to the device
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, P->dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+      cudaGetLastError();
+    }
     ck(cudaStreamCreateWithFlags(&P->nstream, cudaStreamNonBlocking));
     ck(cudaEventCreateWithFlags(&P->ev_perm, cudaEventDisableTiming));
     ck(cudaEventCreateWithFlags(&P->ev_near, cudaEventDisableTiming));

@@ -689,10 +689,14 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
           }
         }
       }
-      if ((int)rows.size() > opt.hf_max_rows) {
+      // sample rows: 6000 at eps >= 1e-4, 6000 more per decade below (tighter selections need more samples
+      // of the wedge's far field; the held-out check below verifies the result); explicit values verbatim
+      const int max_rows = opt.hf_max_rows > 0 ? opt.hf_max_rows
+                                               : 6000 * (1 + (eps < 1e-4 ? (int)std::lround(std::log10(1e-4 / eps)) : 0));
+      if ((int)rows.size() > max_rows) {
         std::mt19937_64 rng(1234567u + 7919u * (uint64_t)rd + 104729u * (uint64_t)l);
         std::shuffle(rows.begin(), rows.end(), rng);
-        rows.resize(opt.hf_max_rows);
+        rows.resize(max_rows);
       }
       // A[i, j] = G(row_i, cand_j) |row_i|: columns J (equivalent points) by pivoted QR of A, then rows I
       // (check points) by pivoted QR of A(:, J)^T

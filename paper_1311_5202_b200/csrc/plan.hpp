@@ -31,7 +31,8 @@ struct Options {
   int lowrank = 1;          // low-rank M2L (eq_lrdk) on/off
   int single_leaf = 0;      // debug: no far field, root is the only leaf (everything P2P)
   int max_depth = 20;
-  int hf_max_rows = 6000;   // HF interpolative-selection sample rows per direction representative
+  int hf_max_rows = 0;      // HF interpolative-selection sample rows per direction representative; 0: 6000 per
+                            // decade of eps from 1e-4 (6000 at eps >= 1e-4)
   double hf_spacing = 0.25; // HF candidate spacing in wavelengths
   int verbose = 0;
   // Translation operators (M2M / L2L / M2L matrices) built on the device (plan_dev.cu) after the host plan:

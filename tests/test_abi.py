@@ -45,7 +45,7 @@ def test_status_strings_and_no_gpu_behaviour():
 def test_options_layout():
     from paper_1311_5202_b200 import fda
     o = fda.fda_options_default()
-    assert o.lowrank == 1 and o.nranks == 1 and o.lf_p_low == 0 and o.hf_max_rows > 0
+    assert o.lowrank == 1 and o.nranks == 1 and o.lf_p_low == 0 and o.hf_max_rows == 0
     assert o.kernel == fda.FDA_KERNEL_BMH and o.eps_lowrank == 0 and o.host_only == 0
     # the struct layout the binding declares matches the C one: a non-default field round-trips
     import numpy as np

@@ -97,6 +97,23 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class stdout_to_stderr:
+    """Send fd 1 to stderr while NCCL initialises (it may print its version on stdout); the bench's one JSON
+    line goes to the real stdout."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def make_inputs(cfg: str, seed: int = 2024):
     p = synth.make_problem(cfg)
     csr = p.correction(seed=seed)
@@ -165,6 +182,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.dist
+    quiet = stdout_to_stderr()
+    quiet.__enter__()
     if use_dist:
         for key_, v_ in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511"), ("RANK", "0"), ("WORLD_SIZE", "1")):
             os.environ.setdefault(key_, v_)
@@ -203,6 +222,9 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    quiet.__exit__(None, None, None)
     # ---- timed region (device time, CUDA events on the launching stream)
     clocks = Clocks(local)
     if world > 1:
@@ -310,8 +332,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms, "apply_s": ms * 1e-3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOADS.get(args.config, args.config), "operator": args.kernel.upper(),
-                           "parallelism": "single GPU" if world == 1 else
-                           f"{world} Morton leaf ranges, NCCL partial-expansion exchange + output all-gather",
+                           "parallelism": "single GPU" if not use_dist else
+                           f"{world} Morton leaf range(s), libfda NCCL partial-expansion exchange + output all-gather",
                            "N": N, "k": p.k, "kD": p.k * float(np.ptp(p.x, axis=0).max()),
                            "eps": p.eps, "alpha": "i/k", "csr_nnz": int(st["csr_nnz"]),
                            "l2": "inputs larger than L2 (correction CSR %.1f GB)" % (st["csr_nnz"] * 20 / 1e9)},

@@ -16,6 +16,7 @@
 #include "nccl_dl.hpp"
 #include "plan.hpp"
 #include "plan_dev.cuh"
+#include "lists_dev.cuh"
 #include "tree_dev.cuh"
 
 using fda::cplx;
@@ -1119,6 +1120,9 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     const bool host_ops = getenv("FDA_HOST_OPS") && getenv("FDA_HOST_OPS")[0] == '1';
     fo.dev_ops = o.host_only || !host_ops || fo.original;
     if (!o.host_only && !host_ops) fo.select = dev_select;
+    // P2 on the device (lists_dev.cu); FDA_HOST_LISTS=1 keeps the host lists (cross-checks)
+    const bool host_lists = getenv("FDA_HOST_LISTS") && getenv("FDA_HOST_LISTS")[0] == '1';
+    if (!o.host_only && !host_lists && !host_ops) fo.lists = fda::build_lists_device;
     std::string err;
     fda::TreeIn tin;
     const double t_dev0 = now();

@@ -992,9 +992,10 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
     // per SM; 32 columns with bulk outputs may take one CTA per SM with FDA_GT_WSP=32)
     static const int wsp = getenv("FDA_GT_WSP") ? atoi(getenv("FDA_GT_WSP")) : 0;
     const bool yb = gt_bulk();
-    // operators too large to stage next to two CTAs per SM (the LF levels): one 512-thread CTA per SM with
-    // the operator staged in shared memory (FDA_GT_WS512=0: off)
-    static const bool ws512 = !(getenv("FDA_GT_WS512") && getenv("FDA_GT_WS512")[0] == '0');
+    // FDA_GT_WS512=1: operators too large to stage next to two CTAs per SM run as one 512-thread CTA per SM
+    // with the operator staged in shared memory.  Measured slower at config 5 (HF level 7: 42.5 vs 35.3 ms;
+    // the LF level's operators do not fit even then), so off by default.
+    static const bool ws512 = getenv("FDA_GT_WS512") && getenv("FDA_GT_WS512")[0] == '1';
     if (ws512 && !yb && !wsp && gt_smem_ws(T, 32, true, false) > budget &&
         gt_smem_ws(T, 32, true, false) <= smem_optin())
       return gt_launch_ws<32, true, false, 512>(T, X, Y, gt_smem_ws(T, 32, true, false), st);

@@ -356,6 +356,13 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     return it == hmap[l].end() ? -1 : it->second;
   };
 
+  // ---- P2 on the device (lists_dev.cu) when the caller provides it: P2P lists, interaction lists, slots and
+  // the M2L groups' pairs; the host code below is the reference (host-only plans, FDA_HOST_LISTS=1)
+  if (opt.lists) {
+    const std::string lerr = opt.lists(P);
+    if (!lerr.empty()) return lerr;
+  }
+  if (!opt.lists) {
   // ---- P2: P2P lists.  Leaf pair (T, S) is direct iff their ancestors at min(lev T, lev S)
   // are adjacent (R20); everything else is covered by exactly one M2L.
   {
@@ -402,6 +409,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
     P.p2p_src.resize(P.p2p_ptr[nl]);
     for (int64_t t = 0; t < nl; ++t) std::copy(src[t].begin(), src[t].end(), P.p2p_src.begin() + P.p2p_ptr[t]);
   }
+  }
 
   // ---- P2: interaction lists per level, grouped by offset (counting sort)
   struct PairL {
@@ -410,7 +418,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   std::vector<std::vector<int32_t>> lv_off_key(nlev);   // per level: offset keys present
   std::vector<std::vector<std::vector<PairL>>> lv_pairs(nlev);  // per level per offset-key-index
   std::vector<std::vector<std::array<int, 3>>> lv_offs(nlev);
-  for (int l = 1; l < nlev; ++l) {
+  for (int l = 1; !opt.lists && l < nlev; ++l) {
     const Level& L = P.levels[l];
     const Level& Lp = P.levels[l - 1];
     const int Rp = Lp.R, Rc = L.R;
@@ -508,7 +516,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   // ---- slots
   const int lmin = P.lmin;
   std::vector<std::vector<int>> grp_dir(nlev);
-  for (int l = 0; l < nlev; ++l) {
+  for (int l = 0; !opt.lists && l < nlev; ++l) {
     Level& L = P.levels[l];
     const int64_t nc = (int64_t)L.cubes.size();
     L.out_slot.assign(nc * L.ndir, -1);
@@ -913,13 +921,13 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   const double tm2m = now();
   // ---- M2L groups: K~ = U_dn^H K V_up = V^T G(delta + b_tgt, b_src) V   (eq_cmpk), low rank (eq_lrdk)
   P.m2l_pool.assign(nlev, {});
-  {
+  if (!opt.lists) {
     size_t tot = 0;
     for (int l = 0; l < nlev; ++l)
       for (const auto& v : lv_pairs[l]) tot += v.size();
     P.m2l_tgt.reserve(tot), P.m2l_src.reserve(tot);
   }
-  for (int l = std::max(lmin, 0); lmin >= 0 && l < nlev; ++l) {
+  for (int l = std::max(lmin, 0); !opt.lists && lmin >= 0 && l < nlev; ++l) {
     Level& L = P.levels[l];
     const int s = L.s;
     const int64_t ng = (int64_t)lv_offs[l].size();

@@ -38,6 +38,8 @@ struct Options {
   // Translation operators (M2M / L2L / M2L matrices) built on the device (plan_dev.cu) after the host plan:
   // build_plan then only records which operators are needed (Trans::need, M2LGroup with rank = -2).
   bool dev_ops = false;
+  // P2 (P2P lists, interaction lists, slots, M2L pairs) built elsewhere (lists_dev.cu); empty: the host code
+  std::function<std::string(struct HostPlan&)> lists;
   // The paper's "original" FDA (Table 1): no SVD reduction of the expansion basis, dense unreduced M2L
   // (requires dev_ops; low rank off)
   bool original = false;

@@ -6,6 +6,8 @@
 * P3 (plan_dev.cu: K~, its low-rank factors, M2M / L2L, the HF directional sets) against the host linear
   algebra (FDA_HOST_OPS=1): the same low-rank / dense decisions and ranks up to a few groups at the
   truncation boundary, and applies that agree to the accuracy of the method (both are ~1e-5 from the oracle).
+* P2 (lists_dev.cu: P2P lists, interaction lists grouped by offset, slots) against the host lists
+  (FDA_HOST_LISTS=1): the same pairs and slots.
 * Invalid inputs and coincident points are rejected by the device P0 as by the host one.
 """
 import os
@@ -65,6 +67,33 @@ def test_device_tree_equals_host_tree(name, nu, k):
         assert all(np.array_equal(x, y) for x, y in zip(fda.fda_plan_export_p2p(hd), fda.fda_plan_export_p2p(hh)))
         assert all(np.array_equal(x, y) for x, y in zip(fda.fda_plan_export_m2l(hd), fda.fda_plan_export_m2l(hh)))
         phi = synth.random_phi(p.N, 3)
+        assert oracle.rel_l2(_apply(hd, phi), _apply(hh, phi)) <= 1e-13
+    finally:
+        fda.fda_plan_destroy(hd)
+        fda.fda_plan_destroy(hh)
+
+
+@pytest.mark.parametrize("name,nu,k", [("hf", 16, 50.0), ("lf", 12, 2.0), ("cfg3", None, None), ("cfg1c", None, None)])
+def test_device_lists_equal_host_lists(name, nu, k):
+    """P2 (lists_dev.cu) against the host lists (FDA_HOST_LISTS=1): the same P2P leaf pairs (arrays equal),
+    the same M2L cube pairs with the same offsets (as sets: the order of equal-target pairs inside a group
+    may differ), the same slot counts, and applies equal to rounding."""
+    fda = _fda()
+    p = synth.make_problem(name[3:]) if name.startswith("cfg") else synth.make_problem("x", k=k, nu=nu)
+    hd = _plan(p)
+    hh = _plan(p, env={"FDA_HOST_LISTS": "1"})
+    try:
+        for x, y in zip(fda.fda_plan_export_p2p(hd), fda.fda_plan_export_p2p(hh)):
+            assert np.array_equal(x, y)
+        md, mh = fda.fda_plan_export_m2l(hd), fda.fda_plan_export_m2l(hh)
+        key = lambda m: np.lexsort(np.column_stack([m[0], m[1], m[2]]).T)  # noqa: E731
+        kd, kh = key(md), key(mh)
+        for x, y in zip(md, mh):
+            assert np.array_equal(x[kd], y[kh])
+        sd, sh = fda.fda_plan_stats(hd), fda.fda_plan_stats(hh)
+        for f in ("m2l_pairs", "m2l_groups", "out_slots", "in_slots", "p2p_point_pairs", "lmin"):
+            assert sd[f] == sh[f], f
+        phi = synth.random_phi(p.N, 7)
         assert oracle.rel_l2(_apply(hd, phi), _apply(hh, phi)) <= 1e-13
     finally:
         fda.fda_plan_destroy(hd)

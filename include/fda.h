@@ -31,7 +31,8 @@
  * Errors: every function returns an fda_status; nothing throws across the ABI.
  *   FDA_ERR_INVALID_ARG   bad sizes / null pointers / non-finite values / |n| != 1 (1e-10) /
  *                         w <= 0 / eps not in [1e-10, 1e-1] / k < 0 / (k == 0 and alpha != 0) /
- *                         CSR with non-monotone row_ptr or col outside [0, n)
+ *                         CSR with non-monotone row_ptr or col outside [0, n) / unknown kernel kind /
+ *                         rank not in [0, nranks) or nranks not in [1, 64]
  *   FDA_ERR_COINCIDENT_POINTS  two distinct points closer than 1e-14 x root width
  *   FDA_ERR_ALIAS         phi and out are the same buffer
  *   FDA_ERR_CUDA          a CUDA error (sticky: destroy the plan)

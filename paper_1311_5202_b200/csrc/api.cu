@@ -1082,7 +1082,7 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
   fda_options_default(&o);
   if (opt) o = *opt;
   if (o.kernel != FDA_KERNEL_BMH && o.kernel != FDA_KERNEL_BMG && o.kernel != FDA_KERNEL_T1) return FDA_ERR_INVALID_ARG;
-  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return FDA_ERR_INVALID_ARG;
+  if (o.nranks < 1 || o.nranks > 64 || o.rank < 0 || o.rank >= o.nranks) return FDA_ERR_INVALID_ARG;
   int ndev = 0;
   if (!o.host_only && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)) {
     cudaGetLastError();

@@ -4,7 +4,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <vector>
 
 #include "plan.hpp"
@@ -265,8 +267,19 @@ void scan_i64(const int64_t* in, int64_t* out, int64_t n) {
 
 }  // namespace
 
+static double ld_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 std::string build_lists_device(HostPlan& P) {
   std::vector<void*> keep;
+  double t0 = ld_now(), t_tab = 0, t_p2p = 0, t_gen = 0, t_slots = 0, t_pairs = 0;
+  auto lap = [&](double& acc) {
+    cudaDeviceSynchronize();
+    const double t = ld_now();
+    acc += t - t0;
+    t0 = t;
+  };
   try {
     const int nlev = (int)P.levels.size();
     // ---- per-level cube tables on the device
@@ -291,6 +304,7 @@ std::string build_lists_device(HostPlan& P) {
       hl[l].child = up(keep, child), hl[l].pbeg = up(keep, pb), hl[l].pend = up(keep, pe);
     }
     const DevLevelT* dlv = up(keep, hl);
+    lap(t_tab);
 
     // ---- P2P lists
     {
@@ -323,6 +337,7 @@ std::string build_lists_device(HostPlan& P) {
       lck(cudaMemcpy(hs.data(), srt.p, tot * sizeof(int32_t), cudaMemcpyDeviceToHost));
       P.p2p_src.assign(hs.begin(), hs.end());
     }
+    lap(t_p2p);
 
     // ---- interaction lists, slots, M2L pairs, level by level
     P.lmin = -1;
@@ -400,6 +415,7 @@ std::string build_lists_device(HostPlan& P) {
           if (P.lmin < 0) P.lmin = l;
         }
       }
+      lap(t_gen);
       const int lmin = P.lmin;
       if (lmin < 0 || l < lmin) continue;
       // groups: offsets and (HF) source wedges
@@ -461,6 +477,7 @@ std::string build_lists_device(HostPlan& P) {
         vd.assign(hd.begin(), hd.end());
         (io ? L.n_in : L.n_out) = ns;
       }
+      lap(t_slots);
       // M2L pairs -> (target in slot, source out slot), groups
       if (np > 0) {
         DBuf<int64_t> tg(np), sr(np);
@@ -481,6 +498,7 @@ std::string build_lists_device(HostPlan& P) {
           P.m2l_groups.push_back(G);
         }
       }
+      lap(t_pairs);
       // the parent level's marks are no longer needed
       if (l >= 1)
         for (void* p : lvl_keep[l - 1]) cudaFree(p);
@@ -489,6 +507,10 @@ std::string build_lists_device(HostPlan& P) {
     for (auto& v : lvl_keep)
       for (void* p : v) cudaFree(p);
     lck(cudaDeviceSynchronize());
+    char buf[256];
+    snprintf(buf, sizeof buf, "lists (device): tables %.3fs p2p %.3fs v-lists %.3fs slots %.3fs pairs %.3fs\n", t_tab,
+             t_p2p, t_gen, t_slots, t_pairs);
+    P.log += buf;
   } catch (const LdFail&) {
     for (void* p : keep) cudaFree(p);
     cudaGetLastError();

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -802,7 +803,11 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   // the HF directional sets must reproduce held-out far fields to the requested accuracy
   for (const Level& L : P.levels)
     for (const DirRep& D : L.reps)
-      if (D.verr > std::max(eps, 20.0 * P.eps_int)) return "SETUP_ACCURACY";
+      if (D.verr > std::max(eps, 20.0 * P.eps_int)) {
+        fprintf(stderr, "[fda] plan: HF wedge %d of level %d (w = %.3g lambda): held-out error %.3g > %.3g\n", D.dir,
+                L.l, k * L.w / (2.0 * PI), D.verr, std::max(eps, 20.0 * P.eps_int));
+        return "SETUP_ACCURACY";
+      }
 
   // point sets of a slot direction (relative to the cube centre)
   auto hf_b = [&](const Level& L, int d) {
@@ -1052,7 +1057,7 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
         << "s m2l " << tm2l - tm2m << "s leaf " << now() - tm2l << "s\n";
     log << "tree " << P.t_tree << "s lists " << P.t_lists << "s ops " << P.t_ops << "s; levels " << nlev
         << " leaves " << P.leaves.size() << " lmin " << lmin << "\n";
-    P.log = log.str();
+    P.log += log.str();
     if (!opt.dev_ops) P.log += level_summary(P);
   }
   return "";

@@ -148,7 +148,14 @@ T* dalloc(fda_plan P, size_t count) {
 template <class T>
 T* upload(fda_plan P, const T* h, size_t count) {
   T* d = dalloc<T>(P, count);
-  if (count) ck(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  if (!count) return d;
+  // large host arrays: pin their pages for the copy (DMA at full PCIe rate instead of the staged path)
+  const size_t bytes = count * sizeof(T);
+  const bool pin = bytes >= (64u << 20) &&
+                   cudaHostRegister(const_cast<T*>(h), bytes, cudaHostRegisterReadOnly) == cudaSuccess;
+  if (bytes >= (64u << 20) && !pin) cudaGetLastError();
+  ck(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+  if (pin) cudaHostUnregister(const_cast<T*>(h));
   return d;
 }
 template <class T>

@@ -232,13 +232,13 @@ __global__ void k_number(int64_t n, int ndir, const unsigned char* __restrict__ 
 }
 __global__ void k_pair_slots(int64_t np, const int64_t* __restrict__ roff, int64_t nruns, const int32_t* __restrict__ gdir,
                              const int32_t* __restrict__ b, const int32_t* __restrict__ c, int m, int ndir, int hf,
-                             const int64_t* __restrict__ islot, const int64_t* __restrict__ oslot, int64_t* tgt,
-                             int64_t* src) {
+                             const int64_t* __restrict__ islot, const int64_t* __restrict__ oslot, int32_t* tgt,
+                             int32_t* src) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= np) return;
   const int d = hf ? gdir[ld_run(roff, nruns, p)] : 0, t = hf ? ld_anti_dir(d, m) : 0;
-  tgt[p] = islot[(int64_t)b[p] * ndir + t];
-  src[p] = oslot[(int64_t)c[p] * ndir + d];
+  tgt[p] = (int32_t)islot[(int64_t)b[p] * ndir + t];
+  src[p] = (int32_t)oslot[(int64_t)c[p] * ndir + d];
 }
 
 template <class T>
@@ -255,6 +255,16 @@ T* up(std::vector<void*>& keep, const std::vector<T>& v) {
   keep.push_back(p);
   if (!v.empty()) lck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   return p;
+}
+
+// device -> host copy of a large result: the destination pages are pinned for the copy (DMA at full PCIe
+// rate instead of the staged pageable path)
+void d2h_pinned(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  const bool pinned = cudaHostRegister(dst, bytes, cudaHostRegisterDefault) == cudaSuccess;
+  if (!pinned) cudaGetLastError();
+  lck(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  if (pinned) cudaHostUnregister(dst);
 }
 
 // exclusive scan of n int64 values into out (n + 1 entries: out[n] = total)
@@ -480,13 +490,13 @@ std::string build_lists_device(HostPlan& P) {
       lap(t_slots);
       // M2L pairs -> (target in slot, source out slot), groups
       if (np > 0) {
-        DBuf<int64_t> tg(np), sr(np);
+        DBuf<int32_t> tg(np), sr(np);
         k_pair_slots<<<ld_nb(np), 256>>>(np, droff, nruns, dgdir, bb->p, oc_s->p, L.m, L.ndir, L.hf ? 1 : 0, islot.p,
                                          oslot.p, tg.p, sr.p);
         const int64_t base = (int64_t)P.m2l_tgt.size();
         P.m2l_tgt.resize(base + np), P.m2l_src.resize(base + np);
-        lck(cudaMemcpy(P.m2l_tgt.data() + base, tg.p, np * sizeof(int64_t), cudaMemcpyDeviceToHost));
-        lck(cudaMemcpy(P.m2l_src.data() + base, sr.p, np * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        d2h_pinned(P.m2l_tgt.data() + base, tg.p, np * sizeof(int32_t));
+        d2h_pinned(P.m2l_src.data() + base, sr.p, np * sizeof(int32_t));
         for (int64_t r = 0; r < nruns; ++r) {
           HostPlan::M2LGroup G;
           G.level = l;

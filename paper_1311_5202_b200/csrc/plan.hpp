@@ -136,7 +136,7 @@ struct HostPlan {
     int64_t mat_off;  // offset (complex elements) into the M2L matrix pool of the level
   };
   std::vector<M2LGroup> m2l_groups;
-  std::vector<int64_t> m2l_tgt, m2l_src;    // slots (in / out) at the group's level
+  std::vector<int32_t> m2l_tgt, m2l_src;    // slots (in / out) at the group's level
   std::vector<std::vector<cplx>> m2l_pool;  // per level
   // M2M / L2L per transition (parent level l): matrices per (dir, octant)
   struct Trans {

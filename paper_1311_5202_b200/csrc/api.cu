@@ -39,6 +39,7 @@ struct DevLevel {
   double2* Y = nullptr;
   fda::GTrans m2l;   // H6 (groups of rank <= the warp-specialised kernel's limit, or all)
   fda::GTrans m2l2;  // H6, remaining groups (higher rank / dense), when the level is split
+  fda::BTrans m2lb;  // H6, low-rank groups (pad8(r) <= 24) with target-owned outputs (m2l_block.cu), launched first
 };
 struct DevTrans {
   int lp = 0, sp = 0, sc = 0;
@@ -105,6 +106,8 @@ struct fda_plan_s {
   std::vector<DevLevel> lv;
   std::vector<DevTrans> tr;
   std::vector<DevLeafOps> lo;
+  double2* tbuf = nullptr;     // two-pass M2L: T = V X of one level's block groups (m2l_block.cu)
+  int64_t tbuf_n = 0;          // complex128 elements (max over levels)
   double2* surfbuf = nullptr;  // check potentials (S2M) / equivalent densities (L2T) of one level's leaves
   int64_t surfbuf_n = 0;
   fda_stats st{};
@@ -391,6 +394,146 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   T.s_out = s_out;
   T.s_in = s_in;
   return T;
+}
+
+// Split a group-major pair set into the groups pred(g) accepts and the others (order kept).
+template <class F>
+void split_groups(const GroupedPairs& G, F pred, GroupedPairs& A, GroupedPairs& B) {
+  const size_t ng = G.rank.size();
+  std::vector<char> ina(ng);
+  std::vector<int64_t> dst(ng);
+  int64_t oa = 0, ob = 0;
+  for (size_t g = 0; g < ng; ++g) {
+    ina[g] = pred(g) ? 1 : 0;
+    GroupedPairs& D = ina[g] ? A : B;
+    const int64_t n = G.gptr[g + 1] - G.gptr[g];
+    D.gptr.push_back(D.gptr.back() + n);
+    D.rank.push_back(G.rank[g]);
+    D.mat.push_back(G.mat[g]);
+    if (!G.so.empty()) D.so.push_back(G.so[g]), D.si.push_back(G.si[g]);
+    dst[g] = ina[g] ? oa : ob;
+    (ina[g] ? oa : ob) += n;
+  }
+  A.out.resize(oa), A.in.resize(oa), B.out.resize(ob), B.in.resize(ob);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t g = 0; g < (int64_t)ng; ++g) {
+    GroupedPairs& D = ina[g] ? A : B;
+    std::copy(G.out.begin() + G.gptr[g], G.out.begin() + G.gptr[g + 1], D.out.begin() + dst[g]);
+    std::copy(G.in.begin() + G.gptr[g], G.in.begin() + G.gptr[g + 1], D.in.begin() + dst[g]);
+  }
+}
+
+// Target blocks of a level's low-rank M2L groups (kernels.cuh BTrans).  The output slots that receive
+// pairs are ordered by (direction, slot) -- slots are numbered cube-major in Morton order, so the slots of
+// one direction are Morton-ordered -- and cut into blocks of <= bmax slots of one direction; the pairs of a
+// block keep the group-major order of G (so they are sorted by group) and are cut into chunks of <= 32
+// pairs of one group.  Blocks launch in the Morton order of their first cube (L2 window of X).
+fda::BTrans make_blocks(fda_plan P, const GroupedPairs& G, const std::vector<int64_t>& out_cube,
+                        const std::vector<int>& out_dir, int s_out, int s_in, const double* dpool) {
+  fda::BTrans B;
+  const int64_t np = (int64_t)G.out.size(), ng = (int64_t)G.rank.size();
+  if (np == 0) return B;
+  int rmax8 = 8;  // >= one row tile (rank-0 groups contribute nothing but keep their chunks)
+  for (int32_t r : G.rank) rmax8 = std::max(rmax8, pad8(r));
+  int bmax = fda::m2l_block_bmax(s_out, rmax8, fda::smem_optin_bytes());
+  if (getenv("FDA_M2L_BMAX")) bmax = std::max(1, std::min(bmax, atoi(getenv("FDA_M2L_BMAX"))));
+  if (bmax <= 0) throw CudaFail{FDA_ERR_SETUP_ACCURACY};
+  const int64_t nslot = (int64_t)out_dir.size();
+  std::vector<int64_t> cnt(nslot, 0);
+  for (int64_t p = 0; p < np; ++p) cnt[G.out[p]]++;
+  std::vector<int32_t> act;
+  for (int64_t sl = 0; sl < nslot; ++sl)
+    if (cnt[sl]) act.push_back((int32_t)sl);
+  std::stable_sort(act.begin(), act.end(), [&](int32_t a, int32_t b) { return out_dir[a] < out_dir[b]; });
+  std::vector<int64_t> sptr{0};
+  std::vector<int32_t> bslot, blk_of(nslot, -1);
+  std::vector<uint8_t> loc_of(nslot, 0);
+  for (size_t i = 0; i < act.size(); ++i) {
+    const int32_t sl = act[i];
+    const int64_t cur = (int64_t)bslot.size() - sptr.back();
+    if (cur == bmax || (cur > 0 && out_dir[bslot.back()] != out_dir[sl])) sptr.push_back((int64_t)bslot.size());
+    blk_of[sl] = (int32_t)(sptr.size() - 1);
+    loc_of[sl] = (uint8_t)((int64_t)bslot.size() - sptr.back());
+    bslot.push_back(sl);
+  }
+  sptr.push_back((int64_t)bslot.size());
+  const int64_t nb = (int64_t)sptr.size() - 1;
+  // pairs by block, stable: group-major inside each block
+  std::vector<int64_t> bp(nb + 1, 0);
+  for (int64_t p = 0; p < np; ++p) bp[blk_of[G.out[p]] + 1]++;
+  for (int64_t b = 0; b < nb; ++b) bp[b + 1] += bp[b];
+  std::vector<int64_t> fill(bp.begin(), bp.end() - 1);
+  std::vector<int32_t> pg(np);
+  std::vector<uint8_t> ploc(np);
+  std::vector<int32_t> p1out(np);  // pass-1 pair (G order) -> pass-2 position
+  for (int64_t g = 0; g < ng; ++g)
+    for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; ++p) {
+      const int32_t o = G.out[p];
+      const int64_t q = fill[blk_of[o]]++;
+      ploc[q] = loc_of[o], pg[q] = (int32_t)g, p1out[p] = (int32_t)q;
+    }
+  std::vector<int64_t> cptr(nb + 1, 0), chp;
+  std::vector<int32_t> chg;
+  std::vector<uint8_t> chl;
+  for (int64_t b = 0; b < nb; ++b) {
+    for (int64_t p = bp[b]; p < bp[b + 1];) {
+      int64_t q = p;
+      while (q < bp[b + 1] && pg[q] == pg[p] && q - p < 32) ++q;
+      chp.push_back(p), chg.push_back(pg[p]);
+      for (int64_t e = 0; e < 32; ++e) chl.push_back(p + e < q ? ploc[p + e] : (uint8_t)0);
+      p = q;
+    }
+    cptr[b + 1] = (int64_t)chg.size();
+  }
+  chp.push_back(np);
+  std::vector<int32_t> order(nb);
+  for (int64_t b = 0; b < nb; ++b) order[b] = (int32_t)b;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    const int64_t ca = out_cube[bslot[sptr[a]]], cb = out_cube[bslot[sptr[b]]];
+    return ca != cb ? ca < cb : out_dir[bslot[sptr[a]]] < out_dir[bslot[sptr[b]]];
+  });
+  // pass-1 items: (group, <= 512 consecutive pairs of G -- sorted by target slot within the group), launched
+  // in the order of their first target: the items resident at any time read the x columns of a narrow Morton
+  // window of sources (L2-resident), while each item reuses its staged V over its pairs
+  std::vector<int32_t> itg0;
+  std::vector<int64_t> itp0;
+  for (int64_t g = 0; g < ng; ++g)
+    for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; p += 512) itg0.push_back((int32_t)g), itp0.push_back(p);
+  std::vector<int32_t> iord(itg0.size());
+  for (size_t i = 0; i < iord.size(); ++i) iord[i] = (int32_t)i;
+  std::stable_sort(iord.begin(), iord.end(), [&](int32_t a, int32_t b) { return G.out[itp0[a]] < G.out[itp0[b]]; });
+  std::vector<int32_t> itg(iord.size());
+  std::vector<int64_t> itp(iord.size() + 1);  // item i: pairs [itp[i], itp_end[i])
+  std::vector<int64_t> ite(iord.size());
+  for (size_t i = 0; i < iord.size(); ++i) {
+    const int32_t k = iord[i];
+    itg[i] = itg0[k], itp[i] = itp0[k];
+    ite[i] = std::min<int64_t>(itp0[k] + 512, G.gptr[itg0[k] + 1]);
+  }
+  itp.pop_back();
+  B.n_blocks = nb;
+  B.n_chunks = (int64_t)chg.size();
+  B.n_pairs = np;
+  B.n_items1 = (int64_t)itg.size();
+  B.blk_order = upload(P, order);
+  B.blk_sptr = upload(P, sptr);
+  B.blk_slot = upload(P, bslot);
+  B.blk_cptr = upload(P, cptr);
+  B.ch_ptr = upload(P, chp);
+  B.ch_group = upload(P, chg);
+  B.ch_loc = upload(P, chl);
+  B.it_group = upload(P, itg);
+  B.it_ptr = upload(P, itp);
+  B.it_end = upload(P, ite);
+  B.p1_in = upload(P, G.in);
+  B.p1_out = upload(P, p1out);
+  B.grank = upload(P, G.rank);
+  B.gmat = upload(P, G.mat);
+  B.pool = dpool;
+  if (!G.so.empty()) B.gso = upload(P, G.so), B.gsi = upload(P, G.si);
+  B.s_out = s_out, B.s_in = s_in, B.rmax8 = rmax8, B.bmax = bmax;
+  B.ldt = fda::m2l_block_ldt(rmax8);
+  return B;
 }
 
 // Ownership (multi-GPU): the leaves (Morton order) are cut into nranks contiguous ranges of
@@ -736,6 +879,35 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->st.flops_m2l += np * (G.rank[g] < 0 ? 8.0 * st_ * ss : 8.0 * G.rank[g] * (st_ + ss));
     }
     const cplx* raw = dev_ops ? nullptr : H.m2l_pool[l].data();
+    // FDA_M2L_BLOCK=1: the low-rank groups with pad8(r) <= 24 (device operators) run as the two-pass M2L with
+    // target-owned outputs (m2l_block.cu: T = V X stored, then Y += U T per target block in shared memory) --
+    // deterministic, but measured slower than the group-major atomic kernels at config 5, so
+    // off by default
+    const bool blk_on = getenv("FDA_M2L_BLOCK") && getenv("FDA_M2L_BLOCK")[0] == '1';  // read per plan (tests toggle it)
+    if (blk_on && dpool) {
+      GroupedPairs Gb, Gr;
+      split_groups(G, [&](size_t g) { return G.rank[g] >= 0 && pad8(G.rank[g]) <= 24; }, Gb, Gr);
+      {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError(), fr = 0;
+        if ((double)Gb.out.size() * fda::m2l_block_ldt(24) * sizeof(double2) > 0.3 * (double)fr) {
+          Gb = GroupedPairs();
+          Gr = G;
+        }
+      }
+      P->lv[l].m2lb = make_blocks(P, Gb, L.in_cube, L.in_dir, L.s, L.s, dpool);
+      P->tbuf_n = std::max<int64_t>(P->tbuf_n, P->lv[l].m2lb.n_pairs * (int64_t)P->lv[l].m2lb.ldt);
+      if (H.opt.verbose && P->lv[l].m2lb.n_blocks) {
+        const fda::BTrans& Bt = P->lv[l].m2lb;
+        std::ostringstream os;
+        os << "m2l blocks L" << l << ": groups " << Gb.rank.size() << "/" << G.rank.size() << " pairs " << Gb.out.size()
+           << " blocks " << Bt.n_blocks << " (<= " << Bt.bmax << " slots) chunks " << Bt.n_chunks << " ("
+           << (double)Gb.out.size() / (double)std::max<int64_t>(1, Bt.n_chunks) << " pairs/chunk) rmax8 " << Bt.rmax8 << "\n";
+        H.log += os.str();
+      }
+      G = std::move(Gr);
+      if (G.out.empty()) continue;
+    }
     // FDA_M2L_MODE=owned|atomic: the item kind of the M2L launches only (experiments; FDA_GT_MODE: all)
     const char* m2l_mode = getenv("FDA_M2L_MODE");
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
@@ -776,6 +948,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
     }
   }
+  if (P->tbuf_n) P->tbuf = dalloc<double2>(P, (size_t)P->tbuf_n);
   lap("m2l");
   // transitions: M2M items own parent out slots (groups = (dir, octant) matrices),
   // L2L items own child in slots (groups = the same matrices, transposed layout)
@@ -1396,9 +1569,16 @@ void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t 
   for (auto& D : P->lv)
     if (D.n_in) ck(cudaMemsetAsync(D.Y, 0, (size_t)D.n_in * D.s * sizeof(double2), st));
   for (size_t l = 0; l < P->lv.size(); ++l) {
+    // stores: before the atomic launches into the same Y
+    if (P->lv[l].m2lb.n_blocks) {
+      ck(fda::launch_m2l_block(P->lv[l].m2lb, P->lv[l].X, P->tbuf, P->lv[l].Y, st, 1));
+      tr(st, "m2l-pass1", (int)l);
+      ck(fda::launch_m2l_block(P->lv[l].m2lb, P->lv[l].X, P->tbuf, P->lv[l].Y, st, 2));
+      tr(st, "m2l-pass2", (int)l);
+    }
     ck(fda::launch_gtrans(P->lv[l].m2l, P->lv[l].X, P->lv[l].Y, st));
     ck(fda::launch_gtrans(P->lv[l].m2l2, P->lv[l].X, P->lv[l].Y, st));
-    if (P->lv[l].m2l.n_items) tr(st, "m2l", (int)l);
+    if (P->lv[l].m2l.n_items || P->lv[l].m2lb.n_blocks) tr(st, "m2l", (int)l);
   }
   mk.end(5);
   mk.begin(6);
@@ -1429,7 +1609,7 @@ int64_t count_launches(fda_plan P, uint32_t mask) {
   if (has_far(P, mask)) {
     for (const auto& O : P->lo) L += 4 * (O.nleaves_own > 0);
     for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
-    for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0);
+    for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0) + 2 * (D.m2lb.n_blocks > 0);
     if (P->nranks > 1) L += (P->xc.nsend > 0) + (P->xc.ndst > 0);
   }
   return L;

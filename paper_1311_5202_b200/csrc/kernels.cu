@@ -904,6 +904,7 @@ static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
     }
   *p = 8, *nbuf = 1, *stage = false;
 }
+size_t smem_optin_bytes() { return smem_optin(); }
 size_t gtrans_smem(const GTrans& T) {
   int p, nb;
   bool stg;

@@ -71,9 +71,49 @@ struct GTrans {
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
 };
 cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
+
+// Two-pass M2L of the low-rank groups (m2l_block.cu).  Pass 1: items (group, <= 2048 pairs) compute
+// T_p = V_o x_s and store it at the pair's position in pass-2 order (ld = ldt).  Pass 2: a block is <= bmax
+// output slots of one direction (Morton-consecutive); its pairs, sorted by group, are cut into chunks of <= 32
+// pairs of one group.  One CTA per block keeps the block's Y rows in shared memory and stores them once:
+// Y[slot] = sum over the block's pairs of U_o T_p (overwrites -- launch it before any atomic contribution to
+// the same Y).
+struct BTrans {
+  int64_t n_blocks = 0, n_chunks = 0, n_pairs = 0, n_items1 = 0;
+  // pass 2
+  const int32_t* blk_order = nullptr;  // launch order (Morton order of the block's first cube)
+  const int64_t* blk_sptr = nullptr;   // block -> [begin, end) into blk_slot
+  const int32_t* blk_slot = nullptr;   // output slots; local index = position - blk_sptr[block]
+  const int64_t* blk_cptr = nullptr;   // block -> [begin, end) into the chunks
+  const int64_t* ch_ptr = nullptr;     // chunk -> [begin, end) into the pass-2 pairs (<= 32) = T columns
+  const int32_t* ch_group = nullptr;   // chunk -> group
+  const uint8_t* ch_loc = nullptr;     // chunk -> 32 local output indices (block-relative) of its pairs
+  // pass 1
+  const int32_t* it_group = nullptr;   // item -> group
+  const int64_t* it_ptr = nullptr;     // item -> [it_ptr, it_end) into the pass-1 pairs (group-major)
+  const int64_t* it_end = nullptr;
+  const int32_t* p1_in = nullptr;      // pass-1 pair -> input slot
+  const int32_t* p1_out = nullptr;     // pass-1 pair -> T column (its pass-2 position)
+  // groups
+  const int32_t* grank = nullptr;      // group -> low rank r (pad8(r) <= 24)
+  const int64_t* gmat = nullptr;       // group -> V (pad8(r) x pad4(s_in)) then U, fragment order (as GTrans)
+  const double* pool = nullptr;
+  const int16_t* gso = nullptr;        // group -> own output / input expansion length (null: s_out / s_in)
+  const int16_t* gsi = nullptr;
+  int s_out = 0, s_in = 0, rmax8 = 0, bmax = 0, ldt = 0;  // ldt: T column stride (complex128), = 4 mod 8
+};
+// pass 1 into T (ldt x n_pairs complex128), then pass 2 into Y (passes: bit 0 pass 1, bit 1 pass 2)
+cudaError_t launch_m2l_block(const BTrans& B, const double2* X, double2* T, double2* Y, cudaStream_t st,
+                             int passes = 3);
+size_t m2l_block_smem(int s_out, int rmax8, int bmax);
+int m2l_block_ldt(int rmax8);
+// largest block (output slots) whose Y rows fit next to the T ring within smem_limit; 0 if rmax8 > 24
+// (those groups stay with launch_gtrans)
+int m2l_block_bmax(int s_out, int rmax8, size_t smem_limit);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
 bool gtrans_fits(const GTrans& T);    // gtrans_smem(T) within the device's opt-in shared-memory limit
 int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)
 int gtrans_ws_rmax(int s_in);         // largest (pad8) low rank the warp-specialised kernel takes
+size_t smem_optin_bytes();            // opt-in shared memory per CTA of the current device
 
 }  // namespace fda

@@ -1,0 +1,9 @@
+#!/bin/bash
+# round 2: two-pass M2L: tests, per-pass trace, ncu (source counters) of the L8 pass 1 and pass 2
+mkdir -p gpurun_out
+python -c "from paper_1311_5202_b200 import build as b; b.build()" > gpurun_out/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_m2l_block.py tests/test_gpu_parity.py -x -q -s -p no:cacheprovider > gpurun_out/pytest_parity.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_parity.log
+FDA_TRACE=1 timeout 900 python bench.py --config 5 --steps 1 --warmup 3 --no-check > /dev/null 2> gpurun_out/trace_raw.log
+grep 'm2l' gpurun_out/trace_raw.log | tail -16 > gpurun_out/trace.log
+timeout 900 ncu --set full --import-source on -k regex:k_m2l_bu --launch-skip 3 --launch-count 1 -o gpurun_out/ncu_bu_l8 python bench.py --config 5 --steps 1 --warmup 1 --no-check > gpurun_out/ncu_bu.log 2>&1
+timeout 900 ncu --set full --import-source on -k regex:k_m2l_tv --launch-skip 3 --launch-count 1 -o gpurun_out/ncu_tv_l8 python bench.py --config 5 --steps 1 --warmup 1 --no-check > gpurun_out/ncu_tv.log 2>&1

@@ -345,7 +345,7 @@ def main():
                 "setup_s": {"inputs": round(t_gen, 2), "plan": round(t_plan, 2), "tree": st["setup_tree_s"],
                             "lists": st["setup_lists_s"], "ops": st["setup_ops_s"], "upload": st["setup_upload_s"]},
                 "plan": {k_: st[k_] for k_ in ("nleaves", "nlevels", "lmin", "p2p_point_pairs", "m2l_pairs",
-                                               "m2l_groups", "m2l_lowrank_groups", "out_slots", "in_slots",
+                                               "m2l_groups", "m2l_lowrank_groups", "m2l_ops", "out_slots", "in_slots",
                                                "device_bytes", "s2m_evals", "l2t_evals", "xchg_send_bytes",
                                                "xchg_recv_bytes")}}
         line["gpu_launches"] = launches_step * args.steps

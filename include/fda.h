@@ -124,6 +124,8 @@ typedef struct {
   double bytes_csr;                                                        /* algorithmic bytes of H3 per apply */
   int64_t s2m_evals, l2t_evals;               /* kernel evaluations of the S2M / L2T surface phases per apply */
   int64_t xchg_send_bytes, xchg_recv_bytes;   /* multi-GPU: expansion bytes this rank sends / receives per apply */
+  int64_t m2l_ops;  /* distinct M2L operators stored: (offset, wedge) groups related by a cube symmetry share one
+                       (the wedges' point sets are rotations of one set), m2l_ops <= m2l_groups */
 } fda_stats;
 
 void fda_options_default(fda_options* opt);

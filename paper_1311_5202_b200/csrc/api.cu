@@ -8,6 +8,7 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -244,6 +245,48 @@ int64_t frag_size(int rank, int s_out, int s_in) {
   return (int64_t)(pad8(rank) / 8) * (pad4(s_in) / 4) * 64 + (int64_t)(pad8(s_out) / 8) * (pad8(rank) / 4) * 64;
 }
 
+// Operators shared by symmetry (HF levels).  The point sets of wedge d are g_d applied to the sets of its
+// orbit representative ("obtained by rotation ... R_up^+ remain the same"; g_d = dir_sym[d],
+// a signed coordinate permutation M_d).  The M2L group (offset delta, source wedge d, target wedge t) has
+//   K[i][j] = G(|delta w + M_t a_i - M_d b_j|) = G(|M_d^T delta w + (M_d^T M_t) a_i - b_j|)
+// (a: target representative's points, b: source representative's), and both reduced bases are the
+// representatives' (R16), so K~ depends only on (rep t, rep d, M_d^T delta, M_d^T M_t): groups with
+// the same key have the same operator, which is built and stored once and applied to the union of their
+// pairs.  LF levels: one point set for every offset, so no sharing.  FDA_M2L_NOSHARE=1 disables it.
+// Returns, per group q of lg, the first q' with the same key (q itself if none).
+std::vector<int32_t> m2l_symmetry_classes(const fda::Level& L, const fda::HostPlan& H, const std::vector<int64_t>& lg,
+                                          const std::vector<int64_t>& cnt) {
+  std::vector<int32_t> cls(lg.size());
+  for (size_t q = 0; q < lg.size(); ++q) cls[q] = (int32_t)q;
+  if (!L.hf || L.dir_sym.empty() || (getenv("FDA_M2L_NOSHARE") && getenv("FDA_M2L_NOSHARE")[0] == '1')) return cls;
+  auto mat = [](const fda::Sym& g, int M[3][3]) {  // (g v)_i = sign_i v_perm_i
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) M[i][j] = (g.perm[i] == j) ? g.sign[i] : 0;
+  };
+  std::map<std::pair<uint64_t, uint64_t>, int32_t> first;
+  for (size_t q = 0; q < lg.size(); ++q) {
+    if (!cnt[q]) continue;
+    const auto& g = H.m2l_groups[lg[q]];
+    const int d = g.dir, t = fda::anti_dir(d, L.m);
+    int Md[3][3], Mt[3][3];
+    mat(L.dir_sym[d], Md), mat(L.dir_sym[t], Mt);
+    const uint64_t reps = (uint64_t)L.dir_rep[d] << 32 | (uint64_t)(uint32_t)L.dir_rep[t];
+    uint64_t key = 0;  // per axis: the offset component (16 bits) and a row of M_d^T M_t (3 trits): 3 x 21 bits
+    for (int i = 0; i < 3; ++i) {
+      int dp = 0;
+      for (int k = 0; k < 3; ++k) dp += Md[k][i] * g.off[k];
+      key = key * (1u << 16) + (uint64_t)(dp + 32768);
+      for (int j = 0; j < 3; ++j) {
+        int h = 0;
+        for (int k = 0; k < 3; ++k) h += Md[k][i] * Mt[k][j];
+        key = key * 3u + (uint64_t)(h + 1);
+      }
+    }
+    cls[q] = first.emplace(std::make_pair(reps, key), (int32_t)q).first->second;
+  }
+  return cls;
+}
+
 // Work items of a grouped translation.  raw != nullptr: the groups' matrices are the host column-major pool
 // raw (G.mat offsets), converted to fragment order and uploaded; raw == nullptr: they are already in the
 // device pool dpool in fragment order (G.mat = offsets in doubles, plan_dev.cu).
@@ -304,9 +347,22 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     std::vector<int64_t> iptr{0}, igpb, igpe;
     std::vector<int32_t> igg, order;
     std::vector<double> cost;
+    // FDA_GT_WIN=W: items also end at the boundaries of W Morton windows of output cubes (equal cube
+    // counts), so the items resident at any time touch the Y rows (and the nearby X rows) of ~one window
+    // and those stay in L2 (experiment)
+    const int64_t W = getenv("FDA_GT_WIN") ? std::max(1, atoi(getenv("FDA_GT_WIN"))) : 1;
+    auto win = [&](int64_t p) { return W == 1 ? 0 : (out_cube[G.out[p]] * W) / std::max<int64_t>(ncubes, 1); };
+    std::vector<int64_t> iwin;
     for (int64_t g = 0; g < ng; ++g)
-      for (int64_t p = G.gptr[g]; p < G.gptr[g + 1]; p += chunk) {
-        const int64_t q = std::min<int64_t>(p + chunk, G.gptr[g + 1]);
+      for (int64_t p = G.gptr[g], q; p < G.gptr[g + 1]; p = q) {
+        q = std::min<int64_t>(p + chunk, G.gptr[g + 1]);
+        if (W > 1) {
+          const int64_t w0 = win(p);
+          if (win(q - 1) != w0) q = std::partition_point(G.out.begin() + p, G.out.begin() + q, [&](int32_t o) {
+                                      return (out_cube[o] * W) / std::max<int64_t>(ncubes, 1) == w0;
+                                    }) - G.out.begin();
+          iwin.push_back(w0);
+        }
         igg.push_back((int32_t)g), igpb.push_back(p), igpe.push_back(q);
         iptr.push_back((int64_t)igg.size());
         const int r = G.rank[g];
@@ -322,6 +378,12 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     const char* io = getenv("FDA_ITEM_ORDER");
     if (io && !strcmp(io, "cost"))
       std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+    else if (W > 1)  // window-major, then Morton (FDA_ITEM_ORDER=group: then the group, then Morton)
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        if (iwin[a] != iwin[b]) return iwin[a] < iwin[b];
+        if (io && !strcmp(io, "group") && igg[a] != igg[b]) return igg[a] < igg[b];
+        return pout[igpb[a]] < pout[igpb[b]];
+      });
     else
       std::stable_sort(order.begin(), order.end(),
                        [&](int32_t a, int32_t b) { return pout[igpb[a]] < pout[igpb[b]]; });
@@ -806,26 +868,53 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       for (int64_t p = g.pbeg; p < g.pend; ++p) c += keep_pair(p);
       cntg[q] = c;
     }
+    // HF levels: groups whose operators are equal by the cube symmetry share one operator (below)
+    const std::vector<int32_t> cls = m2l_symmetry_classes(L, H, lg, cntg);
     GroupedPairs G;
-    std::vector<int64_t> gid;  // group index in H.m2l_groups
-    for (size_t q = 0; q < lg.size(); ++q) {
-      if (!cntg[q]) continue;
-      const auto& g = H.m2l_groups[lg[q]];
-      G.gptr.push_back(G.gptr.back() + cntg[q]);
-      G.rank.push_back(g.rank);
-      G.mat.push_back(g.mat_off);
-      G.so.push_back((int16_t)L.sdir(L.hf ? fda::anti_dir(g.dir, L.m) : 0));
-      G.si.push_back((int16_t)L.sdir(g.dir));
-      gid.push_back(lg[q]);
+    std::vector<int64_t> gid;                 // canonical group (index in H.m2l_groups) of each operator
+    std::vector<std::vector<int64_t>> memb;   // member groups of each operator (level-local indices q)
+    {
+      std::vector<int32_t> slot(lg.size(), -1);
+      for (size_t q = 0; q < lg.size(); ++q) {
+        if (!cntg[q]) continue;
+        int32_t& sl = slot[cls[q]];
+        if (sl < 0) {
+          sl = (int32_t)gid.size();
+          gid.push_back(lg[q]);
+          memb.emplace_back();
+        }
+        memb[sl].push_back((int64_t)q);
+      }
+    }
+    for (size_t g = 0; g < gid.size(); ++g) {
+      const auto& hg = H.m2l_groups[gid[g]];
+      int64_t n = 0;
+      for (int64_t q : memb[g]) n += cntg[q];
+      G.gptr.push_back(G.gptr.back() + n);
+      G.rank.push_back(hg.rank);
+      G.mat.push_back(hg.mat_off);
+      G.so.push_back((int16_t)L.sdir(L.hf ? fda::anti_dir(hg.dir, L.m) : 0));
+      G.si.push_back((int16_t)L.sdir(hg.dir));
     }
     G.out.resize(G.gptr.back()), G.in.resize(G.gptr.back());
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t g = 0; g < (int64_t)gid.size(); ++g) {
-      const auto& hg = H.m2l_groups[gid[g]];
       int64_t o = G.gptr[g];
-      for (int64_t p = hg.pbeg; p < hg.pend; ++p)
-        if (keep_pair(p)) G.out[o] = (int32_t)H.m2l_tgt[p], G.in[o] = (int32_t)H.m2l_src[p], ++o;
+      for (int64_t q : memb[g]) {
+        const auto& hg = H.m2l_groups[lg[q]];
+        for (int64_t p = hg.pbeg; p < hg.pend; ++p)
+          if (keep_pair(p)) G.out[o] = (int32_t)H.m2l_tgt[p], G.in[o] = (int32_t)H.m2l_src[p], ++o;
+      }
+      // a shared operator's pairs in output-slot (Morton) order, as within one group
+      if (memb[g].size() > 1) {
+        std::vector<std::pair<int32_t, int32_t>> pr;
+        pr.reserve(G.gptr[g + 1] - G.gptr[g]);
+        for (int64_t e = G.gptr[g]; e < G.gptr[g + 1]; ++e) pr.emplace_back(G.out[e], G.in[e]);
+        std::sort(pr.begin(), pr.end());
+        for (int64_t e = G.gptr[g]; e < G.gptr[g + 1]; ++e) G.out[e] = pr[e - G.gptr[g]].first, G.in[e] = pr[e - G.gptr[g]].second;
+      }
     }
+    P->st.m2l_ops += (int64_t)gid.size();
     if (G.out.empty()) continue;
     const double* dpool = nullptr;
     if (dev_ops) {
@@ -861,7 +950,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
         off[g] = tot;
         tot += frag_size(rk[g], L.s, L.s);
         G.rank[g] = rk[g], G.mat[g] = off[g];
-        P->H.m2l_groups[gid[g]].rank = rk[g];
+        for (int64_t q : memb[g]) P->H.m2l_groups[lg[q]].rank = rk[g];
       }
       double* pool = dalloc<double>(P, (size_t)tot);
       J.off = upload(P, off), J.pool = pool;
@@ -872,8 +961,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       const auto& hg = H.m2l_groups[gid[g]];
       const double np = (double)(G.gptr[g + 1] - G.gptr[g]);
       P->st.m2l_pairs += (int64_t)np;
-      P->st.m2l_groups += 1;
-      P->st.m2l_lowrank_groups += G.rank[g] >= 0;
+      P->st.m2l_groups += (int64_t)memb[g].size();
+      P->st.m2l_lowrank_groups += G.rank[g] >= 0 ? (int64_t)memb[g].size() : 0;
       // algorithmic flops with the wedges' own expansion lengths (the pool pads them to the level's max)
       const double ss = L.sdir(hg.dir), st_ = L.sdir(L.hf ? fda::anti_dir(hg.dir, L.m) : 0);
       P->st.flops_m2l += np * (G.rank[g] < 0 ? 8.0 * st_ * ss : 8.0 * G.rank[g] * (st_ + ss));

@@ -401,6 +401,9 @@ __device__ __forceinline__ void bulk_issue_cols(double2* Y, const double2* Ys, c
 
 // sector-complete reductions in the atomic epilogue (kernels.cu gt_stage; FDA_GT_SECTOR=1 enables them)
 __constant__ int gt_sector_red = 0;
+// diagnostics only (FDA_GT_NORED=1|2): drop the atomic output of the translations / replace it by plain stores,
+// to measure what the FP64 reductions cost (results are wrong then)
+__constant__ int gt_nored = 0;
 
 __host__ __device__ __forceinline__ int gt_ld(int k) { return ((k + 3) / 8) * 8 + 4; }  // >= k, = 4 mod 8
 
@@ -499,7 +502,9 @@ __device__ __forceinline__ void gt_stage(const double* __restrict__ Ag, int Mt, 
           if (MODE == 2) {
             // rows past the group's own expansion length (an HF wedge shorter than the level's padded s)
             // are exact zeros: no atomic for them
-            if (re != 0.0 || im != 0.0) {
+            if (gt_nored) {  // diagnostics (FDA_GT_NORED): 1 no output, 2 plain stores instead of reductions
+              if (gt_nored == 2 || re == 1.2345e300) *y = make_double2(re, im);
+            } else if (re != 0.0 || im != 0.0) {
               atomicAdd(&y->x, re);
               atomicAdd(&y->y, im);
             }
@@ -981,6 +986,12 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
     return on;
   }();
   (void)sector_on;
+  static const bool nored_on = [] {
+    const int v = getenv("FDA_GT_NORED") ? atoi(getenv("FDA_GT_NORED")) : 0;
+    if (v) cudaMemcpyToSymbol(gt_nored, &v, sizeof(int));
+    return v != 0;
+  }();
+  (void)nored_on;
   // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
   static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
   // owned low-rank items (FDA_GT_MODE=owned): the warp-specialised kernel with plain read-modify-write outputs

@@ -1001,7 +1001,9 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const char* m2l_mode = getenv("FDA_M2L_MODE");
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
     // the nearest offsets) go to a second launch of the general kernel.
-    const int rlim = fda::gtrans_ws_rmax(L.s);
+    // (warp-task kernel: the ranks whose operator keeps two CTAs per SM, m2l_warp.cu)
+    const bool warp = fda::m2l_warp_on();
+    const int rlim = warp ? std::max(8, fda::m2l_warp_rmax(L.s, L.s, GT_SMEM_BUDGET)) : fda::gtrans_ws_rmax(L.s);
     GroupedPairs G1, G2;
     {
       std::vector<char> in1(G.rank.size());
@@ -1036,6 +1038,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     } else {
       P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
     }
+    P->lv[l].m2l.warp_tasks = P->lv[l].m2l2.warp_tasks = warp ? 1 : 0;
   }
   if (P->tbuf_n) P->tbuf = dalloc<double2>(P, (size_t)P->tbuf_n);
   lap("m2l");

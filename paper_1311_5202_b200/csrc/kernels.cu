@@ -364,7 +364,6 @@ void launch_s2m_check(int kind, int64_t nleaves, const int32_t* leaf_ids, LeafGe
 // A warp unit computes (8 rows) x (CT 8-column tiles); CT = GT_P/8 (all the chunk's columns: each A
 // fragment feeds 3*CT DMMAs) for the T stage and the atomic output, CT = 2 for owned outputs (more
 // units -> better balance across warps when the output has few row tiles).
-#define GT_SMEM_BUDGET (112 * 1024)  // per CTA: two CTAs (16 warps) per SM
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -916,7 +915,7 @@ size_t gtrans_smem(const GTrans& T) {
   gt_cfg(T, &p, &nb, &stg);
   return gt_smem(T, p, nb, stg);
 }
-bool gtrans_fits(const GTrans& T) { return T.n_items <= 0 || gtrans_smem(T) <= smem_optin(); }
+bool gtrans_fits(const GTrans& T) { return T.n_items <= 0 || m2l_warp_fits(T) || gtrans_smem(T) <= smem_optin(); }
 int gtrans_cols(const GTrans& T) {
   int p, nb;
   bool stg;
@@ -992,6 +991,8 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
     return v != 0;
   }();
   (void)nored_on;
+  // low-rank M2L items: warp-independent tasks with the operator in shared memory (m2l_warp.cu)
+  if (m2l_warp_fits(T)) return launch_m2l_warp(T, X, Y, st);
   // warp-specialised kernel for all-low-rank atomic items (FDA_GT_WS=0 disables it)
   static const bool ws_ok = !(getenv("FDA_GT_WS") && getenv("FDA_GT_WS")[0] == '0');
   // owned low-rank items (FDA_GT_MODE=owned): the warp-specialised kernel with plain read-modify-write outputs

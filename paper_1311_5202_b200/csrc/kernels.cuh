@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#define GT_SMEM_BUDGET (112 * 1024)  // shared memory per CTA of the translation kernels: two CTAs (16 warps) per SM
+
 namespace fda {
 
 struct LeafGeom {        // leaves in Morton order; leaf t owns points [ptr[t], ptr[t+1])
@@ -69,6 +71,7 @@ struct GTrans {
   int all_lowrank = 0;                  // every group low rank (warp-specialised kernel)
   int ct1 = 0, ct2 = 0;                 // warp-unit column tiles (experiments: FDA_GT_CT1 / FDA_GT_CT2; 0 = default, -1 = balance)
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
+  int warp_tasks = 0;  // 1: low-rank M2L items for the warp-task kernel (m2l_warp.cu; chosen at plan time)
 };
 cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 
@@ -110,6 +113,12 @@ int m2l_block_ldt(int rmax8);
 // largest block (output slots) whose Y rows fit next to the T ring within smem_limit; 0 if rmax8 > 24
 // (those groups stay with launch_gtrans)
 int m2l_block_bmax(int s_out, int rmax8, size_t smem_limit);
+// Low-rank M2L with warp-independent 8-pair tasks and the group's operator staged in shared memory
+// (m2l_warp.cu); launch_gtrans takes it for all-low-rank atomic items when m2l_warp_fits (FDA_M2L_WARP=0: off)
+bool m2l_warp_on();
+bool m2l_warp_fits(const GTrans& T);
+int m2l_warp_rmax(int s_out, int s_in, size_t smem_limit);  // largest pad8 rank whose operator fits smem_limit
+cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 size_t gtrans_smem(const GTrans& T);  // dynamic shared memory of one CTA
 bool gtrans_fits(const GTrans& T);    // gtrans_smem(T) within the device's opt-in shared-memory limit
 int gtrans_cols(const GTrans& T);     // pair columns per chunk (16 or 32)

@@ -292,7 +292,7 @@ std::vector<int32_t> m2l_symmetry_classes(const fda::Level& L, const fda::HostPl
 // device pool dpool in fragment order (G.mat = offsets in doubles, plan_dev.cu).
 fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& out_cube,
                        const std::vector<int>& out_dir, int64_t ncubes, int s_out, int s_in, const cplx* raw,
-                       const double* dpool = nullptr, const char* mode = nullptr) {
+                       const double* dpool = nullptr, const char* mode = nullptr, int win = 0) {
   fda::GTrans T;
   const int64_t ng = (int64_t)G.rank.size(), np = (int64_t)G.out.size();
   if (np == 0) return T;
@@ -350,7 +350,7 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
     // FDA_GT_WIN=W: items also end at the boundaries of W Morton windows of output cubes (equal cube
     // counts), so the items resident at any time touch the Y rows (and the nearby X rows) of ~one window
     // and those stay in L2 (experiment)
-    const int64_t W = getenv("FDA_GT_WIN") ? std::max(1, atoi(getenv("FDA_GT_WIN"))) : 1;
+    const int64_t W = win > 0 ? win : getenv("FDA_GT_WIN") ? std::max(1, atoi(getenv("FDA_GT_WIN"))) : 1;
     auto win = [&](int64_t p) { return W == 1 ? 0 : (out_cube[G.out[p]] * W) / std::max<int64_t>(ncubes, 1); };
     std::vector<int64_t> iwin;
     for (int64_t g = 0; g < ng; ++g)
@@ -499,7 +499,10 @@ fda::BTrans make_blocks(fda_plan P, const GroupedPairs& G, const std::vector<int
   for (int32_t r : G.rank) rmax8 = std::max(rmax8, pad8(r));
   int bmax = fda::m2l_block_bmax(s_out, rmax8, fda::smem_optin_bytes());
   if (getenv("FDA_M2L_BMAX")) bmax = std::max(1, std::min(bmax, atoi(getenv("FDA_M2L_BMAX"))));
-  if (bmax <= 0) throw CudaFail{FDA_ERR_SETUP_ACCURACY};
+  if (bmax <= 0) {
+    fprintf(stderr, "fda: target-block M2L: no block fits (s_out %d, rmax8 %d)\n", s_out, rmax8);
+    throw CudaFail{FDA_ERR_SETUP_ACCURACY};
+  }
   const int64_t nslot = (int64_t)out_dir.size();
   std::vector<int64_t> cnt(nslot, 0);
   for (int64_t p = 0; p < np; ++p) cnt[G.out[p]]++;
@@ -975,7 +978,9 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const bool blk_on = getenv("FDA_M2L_BLOCK") && getenv("FDA_M2L_BLOCK")[0] == '1';  // read per plan (tests toggle it)
     if (blk_on && dpool) {
       GroupedPairs Gb, Gr;
-      split_groups(G, [&](size_t g) { return G.rank[g] >= 0 && pad8(G.rank[g]) <= 24; }, Gb, Gr);
+      // (a level whose expansions are too long for the block kernel's shared memory keeps every group in Gr)
+      const bool blk_fits = fda::m2l_block_bmax(L.s, 24, fda::smem_optin_bytes()) > 0;
+      split_groups(G, [&](size_t g) { return blk_fits && G.rank[g] >= 0 && pad8(G.rank[g]) <= 24; }, Gb, Gr);
       {
         size_t fr = 0, tot = 0;
         if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError(), fr = 0;
@@ -1001,9 +1006,12 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     const char* m2l_mode = getenv("FDA_M2L_MODE");
     // Groups whose rank fits the warp-specialised kernel's shared memory run there; the others (few,
     // the nearest offsets) go to a second launch of the general kernel.
-    // (warp-task kernel: the ranks whose operator keeps two CTAs per SM, m2l_warp.cu)
     const bool warp = fda::m2l_warp_on();
-    const int rlim = warp ? std::max(8, fda::m2l_warp_rmax(L.s, L.s, GT_SMEM_BUDGET)) : fda::gtrans_ws_rmax(L.s);
+    // (warp-task kernel: ranks <= 24 whose operator keeps two CTAs per SM go to the first launch, the others to
+    // the second; measured at config 5 (profiles/r02/ab_c5.log): M2L 158.2 ms with the split at 24, 162.8 ms with
+    // the ranks <= 16 in a three-CTAs-per-SM launch of their own; FDA_M2L_RLIM overrides it)
+    int rlim = warp ? std::max(8, std::min(24, fda::m2l_warp_rmax(L.s, L.s, GT_SMEM_BUDGET))) : fda::gtrans_ws_rmax(L.s);
+    if (warp && getenv("FDA_M2L_RLIM")) rlim = std::max(8, atoi(getenv("FDA_M2L_RLIM")));
     GroupedPairs G1, G2;
     {
       std::vector<char> in1(G.rank.size());
@@ -1032,13 +1040,16 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
         }
       }
     }
+    // FDA_M2L_WIN=W (experiment): the LF levels' items end at W Morton windows of target cubes (L2 residency of Y)
+    const int win = (!L.hf && getenv("FDA_M2L_WIN")) ? atoi(getenv("FDA_M2L_WIN")) : 0;
     if (!G1.rank.empty() && !G2.rank.empty()) {
-      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
-      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
+      P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode, win);
+      P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode, win);
     } else {
-      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode);
+      P->lv[l].m2l = make_items(P, G, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode, win);
     }
     P->lv[l].m2l.warp_tasks = P->lv[l].m2l2.warp_tasks = warp ? 1 : 0;
+    P->lv[l].m2l.sector = P->lv[l].m2l2.sector = 0;  // measured slower at config 5 (ab_c5.log: +4.7 ms)
   }
   if (P->tbuf_n) P->tbuf = dalloc<double2>(P, (size_t)P->tbuf_n);
   lap("m2l");
@@ -1199,7 +1210,10 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     for (const auto& D : P->lv) fits &= fda::gtrans_fits(D.m2l) && fda::gtrans_fits(D.m2l2);
     for (const auto& T : P->tr) fits &= fda::gtrans_fits(T.up) && fda::gtrans_fits(T.dn);
     for (const auto& O : P->lo) fits &= fda::gtrans_fits(O.s2m) && fda::gtrans_fits(O.l2t);
-    if (!fits) return FDA_ERR_SETUP_ACCURACY;
+    if (!fits) {
+      fprintf(stderr, "fda: a translation launch exceeds the device's shared memory per CTA\n");
+      return FDA_ERR_SETUP_ACCURACY;
+    }
   }
   // stats
   fda_stats& s = P->st;

@@ -72,6 +72,7 @@ struct GTrans {
   int ct1 = 0, ct2 = 0;                 // warp-unit column tiles (experiments: FDA_GT_CT1 / FDA_GT_CT2; 0 = default, -1 = balance)
   int atomic = 0;   // 1: items are (group, pair chunk) and accumulate with atomics (few pairs per group)
   int warp_tasks = 0;  // 1: low-rank M2L items for the warp-task kernel (m2l_warp.cu; chosen at plan time)
+  int sector = 0;      // warp-task kernel: sector-complete FP64 reductions (the plan sets it on the LF levels)
 };
 cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStream_t st);
 

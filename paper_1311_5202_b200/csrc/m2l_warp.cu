@@ -34,22 +34,30 @@ constexpr int MW_D = 4;    // k tiles of x prefetched ahead
 // One task: the (up to) 8 pairs [p0, pe) of a group whose V has RT row tiles (pad8(r) = 8 RT).
 //   Ms: the staged operator; kin: k tiles per row tile of V (level s_in); kt1: k tiles of the group's own
 //   input length; mo: row tiles of the group's own output length; kt2: k tiles of U holding the rank r.
-template <int RT>
+template <int RT, int NS, int SEC>
 __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin, int kt1, int mo, int kt2, int s_in,
-                                         int s_out, const double2* __restrict__ X, double2* __restrict__ Y,
+                                         int s_out, int so_own, const double2* __restrict__ X, double2* __restrict__ Y,
                                          const int32_t* __restrict__ pin, const int32_t* __restrict__ pout,
                                          int64_t p0, int64_t pe, int lane) {
   const int g = lane >> 2, t = lane & 3;
   // B operand of stage 1: lane (g, t) holds x[k = 4 kt + t] of pair column g
   const int in_slot = p0 + g < pe ? pin[p0 + g] : -1;
   const double2* xs = X + (int64_t)(in_slot < 0 ? 0 : in_slot) * s_in;
+  // predicated load into zeroed registers (a select on the loaded value would wait for the load at once)
   auto ldx = [&](int kt) {
     const int k = 4 * kt + t;
-    return (in_slot >= 0 && kt < kt1 && k < s_in) ? __ldg(xs + k) : make_double2(0.0, 0.0);
+    double2 v = make_double2(0.0, 0.0);
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p ld.global.nc.v2.f64 {%0, %1}, [%3];\n}\n"
+        : "+d"(v.x), "+d"(v.y)
+        : "r"((int)(in_slot >= 0 && kt < kt1 && k < s_in)), "l"(xs + k));
+    return v;
   };
-  // output slots of the accumulator columns 2t, 2t + 1
-  const int o0 = p0 + 2 * t < pe ? pout[p0 + 2 * t] : -1;
-  const int o1 = p0 + 2 * t + 1 < pe ? pout[p0 + 2 * t + 1] : -1;
+  // output slots: SEC == 0, of the accumulator columns 2t, 2t + 1; SEC == 1, of the columns 2 (lane >> 3) + j
+  // that this lane reduces into in the sector-complete epilogue
+  const int cb = SEC ? 2 * (lane >> 3) : 2 * t;
+  const int o0 = p0 + cb < pe ? pout[p0 + cb] : -1;
+  const int o1 = p0 + cb + 1 < pe ? pout[p0 + cb + 1] : -1;
 
   double acc[RT][3][2];
 #pragma unroll
@@ -70,10 +78,11 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
         const double bs = b.x + b.y;
 #pragma unroll
         for (int i = 0; i < RT; ++i) {
-          const double ar = vl[(i * kin + kt) * 64], ai = vl[(i * kin + kt) * 64 + 32];
+          const double* a = vl + (i * kin + kt) * NS;
+          const double ar = a[0], ai = a[32], as = NS == 96 ? a[64] : ar + ai;
           dmma_w(acc[i][0][0], acc[i][0][1], ar, b.x);
           dmma_w(acc[i][1][0], acc[i][1][1], ai, b.y);
-          dmma_w(acc[i][2][0], acc[i][2][1], ar + ai, bs);
+          dmma_w(acc[i][2][0], acc[i][2][1], as, bs);
         }
       }
     }
@@ -101,36 +110,64 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
     }
   }
   // stage 2: per output row tile, Y[out] += U T
-  const double* ul = Ms + (size_t)RT * kin * 64 + lane;
+  const double* ul = Ms + (size_t)RT * kin * NS + lane;
   for (int mt = 0; mt < mo; ++mt) {
     double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int kk = 0; kk < 2 * RT; ++kk) {
       if (kk < kt2) {
-        const double ar = ul[(mt * 2 * RT + kk) * 64], ai = ul[(mt * 2 * RT + kk) * 64 + 32];
+        const double* a = ul + (mt * 2 * RT + kk) * NS;
+        const double ar = a[0], ai = a[32], as = NS == 96 ? a[64] : ar + ai;
         dmma_w(c[0][0], c[0][1], ar, br[kk]);
         dmma_w(c[1][0], c[1][1], ai, bi[kk]);
-        dmma_w(c[2][0], c[2][1], ar + ai, bsum[kk]);
+        dmma_w(c[2][0], c[2][1], as, bsum[kk]);
       }
     }
-    const int row = mt * 8 + g;
-    if (row < s_out) {
+    // rows past the group's own output length (a short HF wedge) are exact zeros: no reduction for them
+    if (!SEC) {
+      const int row = mt * 8 + g;
+      if (row < so_own) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int o = j ? o1 : o0;
-        const double re = c[0][j] - c[1][j], im = c[2][j] - c[0][j] - c[1][j];
-        if (o >= 0 && (re != 0.0 || im != 0.0)) {
-          double2* y = Y + (int64_t)o * s_out + row;
-          atomicAdd(&y->x, re);
-          atomicAdd(&y->y, im);
+        for (int j = 0; j < 2; ++j) {
+          const int o = j ? o1 : o0;
+          const double re = c[0][j] - c[1][j], im = c[2][j] - c[0][j] - c[1][j];
+          if (o >= 0) {
+            double2* y = Y + (int64_t)o * s_out + row;
+            atomicAdd(&y->x, re);
+            atomicAdd(&y->y, im);
+          }
         }
       }
+    } else {
+      // Sector-complete reductions: the L2 applies FP64 reductions per 32-byte sector, and a lane's own values
+      // (re or im of one row, two columns) fill half a sector per instruction.  Shuffled so that lanes 4q..4q+3
+      // add (re, im) of rows 2h, 2h + 1 of one column -- one whole sector (s_out even, so every row pair starts a
+      // sector): 4 instructions per row tile touch 32 sectors instead of 64.  Instruction (j, half): column
+      // 2 (lane >> 3) + j, row pair h = 2 half + ((lane >> 2) & 1), element e = lane & 3 (re/im of row 2h + e/2).
+      double re[2], im[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) re[j] = c[0][j] - c[1][j], im[j] = c[2][j] - c[0][j] - c[1][j];
+      const int e = lane & 3, tq = lane >> 3, hh = (lane >> 2) & 1;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int h = 2 * half + hh, rr = 2 * h + (e >> 1);
+          const int src = rr * 4 + tq;
+          const double vr = __shfl_sync(0xffffffffu, re[j], src), vi = __shfl_sync(0xffffffffu, im[j], src);
+          const int o = j ? o1 : o0, row = mt * 8 + rr;
+          if (o >= 0 && row < so_own)
+            atomicAdd(reinterpret_cast<double*>(Y + (int64_t)o * s_out + row) + (e & 1), (e & 1) ? vi : vr);
+        }
     }
   }
 }
 
-__global__ void __launch_bounds__(MW_T, 2) k_m2l_warp(GTrans T, const double2* __restrict__ X,
-                                                      double2* __restrict__ Y) {
+// NS: doubles per staged operator tile (64, or 96 with the 3M sums); RTMAX: largest V row-tile count of the
+// launch's groups; MINB: CTAs per SM the registers are budgeted for
+template <int NS, int RTMAX, int MINB, int SEC>
+__global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2* __restrict__ X,
+                                                         double2* __restrict__ Y) {
   extern __shared__ double msm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s_in = T.s_in, s_out = T.s_out;
@@ -139,28 +176,39 @@ __global__ void __launch_bounds__(MW_T, 2) k_m2l_warp(GTrans T, const double2* _
   for (int64_t e = T.item_ptr[item]; e < T.item_ptr[item + 1]; ++e) {
     const int grp = T.ig_group[e];
     const int rank = T.grank[grp], rt = (rank + 7) / 8;
-    const int kt1 = T.gsi ? (T.gsi[grp] + 3) / 4 : kin, mo = T.gso ? (T.gso[grp] + 7) / 8 : mout;
+    const int so_own = T.gso ? T.gso[grp] : s_out;
+    const int kt1 = T.gsi ? (T.gsi[grp] + 3) / 4 : kin, mo = (so_own + 7) / 8;
     const int kt2 = (rank + 3) / 4;
     if (rt <= 0) continue;  // rank 0: nothing to add
     // stage the group's operator (V then U, fragment order, contiguous)
     __syncthreads();  // the previous group's operator is no longer read
     {
       const double* src = T.pool + T.gmat[grp];
-      const int nd = (rt * kin + mout * 2 * rt) * 64;
-      for (int i = tid; i < nd / 2; i += MW_T) cp_async16_w(msm + 2 * i, src + 2 * i);
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      const int ntile = rt * kin + mout * 2 * rt;
+      if (NS == 64) {
+        for (int i = tid; i < ntile * 32; i += MW_T) cp_async16_w(msm + 2 * i, src + 2 * i);
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      } else {  // tiles of 96: the real and imaginary parts and their sum (the 3M operand), summed once here
+        for (int i = tid; i < ntile * 32; i += MW_T) {
+          const int q = i >> 5, l = i & 31;
+          const double re = __ldg(src + q * 64 + l), im = __ldg(src + q * 64 + 32 + l);
+          msm[q * 96 + l] = re, msm[q * 96 + 32 + l] = im, msm[q * 96 + 64 + l] = re + im;
+        }
+      }
     }
     __syncthreads();
     const int64_t pb = T.ig_pb[e], pe = T.ig_pe[e];
     const int64_t ntask = (pe - pb + 7) / 8;
     for (int64_t task = warp; task < ntask; task += MW_T / 32) {
       const int64_t p0 = pb + 8 * task;
-      switch (rt) {
-        case 1: m2l_task<1>(msm, kin, kt1, mo, kt2, s_in, s_out, X, Y, T.in, T.out, p0, pe, lane); break;
-        case 2: m2l_task<2>(msm, kin, kt1, mo, kt2, s_in, s_out, X, Y, T.in, T.out, p0, pe, lane); break;
-        case 3: m2l_task<3>(msm, kin, kt1, mo, kt2, s_in, s_out, X, Y, T.in, T.out, p0, pe, lane); break;
-        default: m2l_task<4>(msm, kin, kt1, mo, kt2, s_in, s_out, X, Y, T.in, T.out, p0, pe, lane); break;
-      }
+      if (rt == 1 || RTMAX == 1)
+        m2l_task<1, NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+      else if (rt == 2 || RTMAX == 2)
+        m2l_task<(RTMAX >= 2 ? 2 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+      else if (rt == 3 || RTMAX == 3)
+        m2l_task<(RTMAX >= 3 ? 3 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+      else
+        m2l_task<(RTMAX >= 4 ? 4 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
     }
   }
 }
@@ -187,12 +235,30 @@ bool m2l_warp_fits(const GTrans& T) {
 
 cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return cudaSuccess;
-  const size_t sm = (size_t)T.mmax * sizeof(double);
+  // Configuration: three CTAs per SM (24 warps: more latency hiding; registers budgeted for RTMAX <= 2) when the
+  // operator fits a third of the shared memory, else two; the tiles carry the 3M sums when those still fit
+  // (FDA_M2L_SUM3=0: never; FDA_M2L_OCC=2: at most two CTAs per SM)
+  const size_t sm2 = (size_t)T.mmax * sizeof(double), sm3 = sm2 * 3 / 2;
+  const size_t third = 74 * 1024;
+  const bool allow3 = !(getenv("FDA_M2L_SUM3") && getenv("FDA_M2L_SUM3")[0] == '0');
+  const bool occ3 = T.rmax8 <= 16 && sm2 <= third && !(getenv("FDA_M2L_OCC") && getenv("FDA_M2L_OCC")[0] == '2');
+  const bool sum3 = allow3 && sm3 <= (occ3 ? third : (size_t)GT_SMEM_BUDGET);
+  const size_t sm = sum3 ? sm3 : sm2;
+  // sector-complete reductions on the launches the plan marked (none by default: measured at config 5, M2L
+  // 162.8 ms with them on the LF level against 158.2 without, profiles/r02/ab_c5.log); they need an even s_out.
+  // FDA_M2L_SECTOR=0 / 2: never / on every level
+  const char* se = getenv("FDA_M2L_SECTOR");
+  const bool sec = T.s_out % 2 == 0 && (se ? se[0] == '2' || (se[0] != '0' && T.sector) : T.sector);
+  void (*kern)(GTrans, const double2*, double2*) =
+      sec ? (occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 1> : k_m2l_warp<64, 2, 3, 1>)
+                  : (sum3 ? k_m2l_warp<96, 4, 2, 1> : k_m2l_warp<64, 4, 2, 1>))
+          : (occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 0> : k_m2l_warp<64, 2, 3, 0>)
+                  : (sum3 ? k_m2l_warp<96, 4, 2, 0> : k_m2l_warp<64, 4, 2, 0>));
   if (sm > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_m2l_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_m2l_warp<<<(unsigned)T.n_items, MW_T, sm, st>>>(T, X, Y);
+  kern<<<(unsigned)T.n_items, MW_T, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
 

@@ -5,7 +5,7 @@
 // (V: pad8(r) x s_in, then U: s_out x pad8(r), DMMA fragment order, api.cu frag_pool) is staged once in shared
 // memory; then every warp works alone on tasks of 8 pairs, with no CTA barrier until the next group:
 //   stage 1  T (pad8(r) x 8) = V X      A = V from shared memory, B = the 8 x columns read straight from
-//                                        global memory (L2) into registers, prefetched 4 k tiles ahead
+//                                        global memory (L2) into registers, prefetched 4-8 k tiles ahead
 //   shuffle  T from the accumulator layout into the B-operand layout of stage 2 (registers only)
 //   stage 2  Y[out] += U T              A = U from shared memory, per 8-row tile of the output; FP64
 //                                        reductions (REDG) of the non-zero rows into Y
@@ -29,12 +29,11 @@ __device__ __forceinline__ void cp_async16_w(void* smem, const void* gmem) {
 }
 
 constexpr int MW_T = 256;  // threads per CTA (8 warps)
-constexpr int MW_D = 4;    // k tiles of x prefetched ahead
 
 // One task: the (up to) 8 pairs [p0, pe) of a group whose V has RT row tiles (pad8(r) = 8 RT).
 //   Ms: the staged operator; kin: k tiles per row tile of V (level s_in); kt1: k tiles of the group's own
 //   input length; mo: row tiles of the group's own output length; kt2: k tiles of U holding the rank r.
-template <int RT, int NS, int SEC>
+template <int RT, int NS, int SEC, int MW_D>
 __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin, int kt1, int mo, int kt2, int s_in,
                                          int s_out, int so_own, const double2* __restrict__ X, double2* __restrict__ Y,
                                          const int32_t* __restrict__ pin, const int32_t* __restrict__ pout,
@@ -43,15 +42,16 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
   // B operand of stage 1: lane (g, t) holds x[k = 4 kt + t] of pair column g
   const int in_slot = p0 + g < pe ? pin[p0 + g] : -1;
   const double2* xs = X + (int64_t)(in_slot < 0 ? 0 : in_slot) * s_in;
-  // predicated load into zeroed registers (a select on the loaded value would wait for the load at once)
-  auto ldx = [&](int kt) {
+  // x prefetch ring bq[0..D): slot d holds the B fragment of k tile kt + d; refilled in place by a predicated
+  // load into the zeroed slot right after its use, so the loop carries no register moves that would wait on a
+  // load (a select or copy of the loaded value would)
+  auto ldx = [&](double2& v, int kt) {
     const int k = 4 * kt + t;
-    double2 v = make_double2(0.0, 0.0);
+    v.x = 0.0, v.y = 0.0;
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p ld.global.nc.v2.f64 {%0, %1}, [%3];\n}\n"
         : "+d"(v.x), "+d"(v.y)
         : "r"((int)(in_slot >= 0 && kt < kt1 && k < s_in)), "l"(xs + k));
-    return v;
   };
   // output slots: SEC == 0, of the accumulator columns 2t, 2t + 1; SEC == 1, of the columns 2 (lane >> 3) + j
   // that this lane reduces into in the sector-complete epilogue
@@ -64,29 +64,37 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
   for (int i = 0; i < RT; ++i)
 #pragma unroll
     for (int q = 0; q < 3; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
-  double2 bq[MW_D];
+  // two halves of MW_D slots, used alternately: a half is refilled (k tiles + MW_D) while the other is consumed,
+  // so no load targets a register an in-flight DMMA of the same half still reads
+  double2 bq[2 * MW_D];
 #pragma unroll
-  for (int d = 0; d < MW_D; ++d) bq[d] = ldx(d);
+  for (int d = 0; d < 2 * MW_D; ++d) ldx(bq[d], d);
   const double* vl = Ms + lane;
-  for (int kt0 = 0; kt0 < kt1; kt0 += MW_D) {
+  auto step = [&](const double2 b, int kt) {
+    const double bs = b.x + b.y;
 #pragma unroll
-    for (int d = 0; d < MW_D; ++d) {
-      const int kt = kt0 + d;
-      if (kt < kt1) {
-        const double2 b = bq[d];
-        bq[d] = ldx(kt + MW_D);
-        const double bs = b.x + b.y;
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const double* a = vl + (i * kin + kt) * NS;
-          const double ar = a[0], ai = a[32], as = NS == 96 ? a[64] : ar + ai;
-          dmma_w(acc[i][0][0], acc[i][0][1], ar, b.x);
-          dmma_w(acc[i][1][0], acc[i][1][1], ai, b.y);
-          dmma_w(acc[i][2][0], acc[i][2][1], as, bs);
-        }
-      }
+    for (int i = 0; i < RT; ++i) {
+      const double* a = vl + (i * kin + kt) * NS;
+      const double ar = a[0], ai = a[32], as = NS == 96 ? a[64] : ar + ai;
+      dmma_w(acc[i][0][0], acc[i][0][1], ar, b.x);
+      dmma_w(acc[i][1][0], acc[i][1][1], ai, b.y);
+      dmma_w(acc[i][2][0], acc[i][2][1], as, bs);
     }
+  };
+  int kt0 = 0;
+  for (; kt0 + 2 * MW_D <= kt1; kt0 += 2 * MW_D) {
+#pragma unroll
+    for (int d = 0; d < MW_D; ++d) step(bq[d], kt0 + d);
+#pragma unroll
+    for (int d = 0; d < MW_D; ++d) ldx(bq[d], kt0 + 2 * MW_D + d);
+#pragma unroll
+    for (int d = MW_D; d < 2 * MW_D; ++d) step(bq[d], kt0 + d);
+#pragma unroll
+    for (int d = MW_D; d < 2 * MW_D; ++d) ldx(bq[d], kt0 + 2 * MW_D + d);
   }
+#pragma unroll
+  for (int d = 0; d < 2 * MW_D; ++d)
+    if (kt0 + d < kt1) step(bq[d], kt0 + d);
   // T = V X: lane (g, t) holds T[8 i + g][2 t + j]; stage 2 needs, for k tile kk, T[4 kk + t][g] -- held by
   // lane (4 (kk & 1) + t) * 4 + (g >> 1), element j = g & 1 of row tile kk >> 1
   double br[2 * RT], bi[2 * RT], bsum[2 * RT];
@@ -202,13 +210,13 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
     for (int64_t task = warp; task < ntask; task += MW_T / 32) {
       const int64_t p0 = pb + 8 * task;
       if (rt == 1 || RTMAX == 1)
-        m2l_task<1, NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<1, NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 2 || RTMAX == 2)
-        m2l_task<(RTMAX >= 2 ? 2 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 2 ? 2 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 3 || RTMAX == 3)
-        m2l_task<(RTMAX >= 3 ? 3 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 3 ? 3 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else
-        m2l_task<(RTMAX >= 4 ? 4 : 1), NS, SEC>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 4 ? 4 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
     }
   }
 }

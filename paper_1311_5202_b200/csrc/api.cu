@@ -937,6 +937,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       J.a = upload(P, ia), J.b = upload(P, ib), J.shift = upload(P, sh);
       J.sets = d_sets, J.k = H.k, J.s_out = L.s, J.s_in = L.s;
       J.compress = H.opt.lowrank ? 1 : 0, J.eps_lr = H.eps_lr_level(L);
+      // FDA_RANK_ROUND=n (experiments): round the low ranks up to a multiple of n instead of 8
+      if (getenv("FDA_RANK_ROUND")) J.rank_round = std::max(1, atoi(getenv("FDA_RANK_ROUND")));
       set_max(bset[l], &J.maxn);
       J.maxs = L.s;
       std::vector<int32_t> rk(ng, -1);

@@ -268,7 +268,8 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
           if (sig[sel[i]] >= J.eps_lr * s1 && sig[sel[i]] > 0.0) ++r;
         // low rank iff r < s/2 (eq_lrdk); the kernel computes with r rounded up to 8 (its tile height), so
         // the rank is rounded up too -- more accuracy at no extra work (R23)
-        const int r8 = min((r + 7) / 8 * 8, np_);
+        const int rr = J.rank_round > 1 ? J.rank_round : 1;
+        const int r8 = min((r + rr - 1) / rr * rr, np_);
         s_rank = (2 * r < max(sA, sB)) ? (2 * r8 < max(sA, sB) ? r8 : r) : -1;
       }
       __syncthreads();

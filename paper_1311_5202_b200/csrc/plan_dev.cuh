@@ -38,6 +38,7 @@ struct OpJob {
   // M2L compression
   int compress = 0;              // 1: pivoted MGS + SVD, low rank iff 2 r < max(s_A, s_B)
   double eps_lr = 0;
+  int rank_round = 8;            // the rank is rounded up to a multiple of this (R23)
   int32_t* rank = nullptr;       // pass 1 output: r, or -1 for dense
   const int32_t* rank_in = nullptr;  // pass 2 input (from pass 1)
   const int64_t* off = nullptr;  // pass 2: item -> offset (doubles) into pool

@@ -135,16 +135,24 @@ struct CudaFail {
   fda_status s;
 };
 
-void ck(cudaError_t e) {
+// FDA_DEBUG=1: report the failing call site on stderr
+void ck_at(cudaError_t e, int line) {
+  if (e == cudaSuccess) return;
+  if (getenv("FDA_DEBUG")) fprintf(stderr, "fda: CUDA error %s at api.cu:%d\n", cudaGetErrorString(e), line);
   if (e == cudaErrorMemoryAllocation) throw CudaFail{FDA_ERR_OOM};
-  if (e != cudaSuccess) throw CudaFail{FDA_ERR_CUDA};
+  throw CudaFail{FDA_ERR_CUDA};
 }
+#define ck(e) ck_at((e), __LINE__)
 
 template <class T>
 T* dalloc(fda_plan P, size_t count) {
   if (count == 0) count = 1;
   void* p = nullptr;
-  ck(cudaMalloc(&p, count * sizeof(T)));
+  const cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess && getenv("FDA_DEBUG"))
+    fprintf(stderr, "fda: cudaMalloc of %zu bytes failed (plan holds %lld bytes)\n", count * sizeof(T),
+            (long long)P->bytes);
+  ck(e);
   P->allocs.push_back(p);
   P->bytes += (int64_t)(count * sizeof(T));
   return (T*)p;
@@ -851,7 +859,8 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     P->dev_sets = hs;
   }
   auto set_max = [&](const std::vector<int>& ids, int* maxn) {
-    for (int i : ids) *maxn = std::max(*maxn, P->dev_sets[i].n);
+    for (int i : ids)  // (directions without a set have id -1)
+      if (i >= 0) *maxn = std::max(*maxn, P->dev_sets[i].n);
   };
   lap("sets");
   // M2L: pairs filtered to owned targets, grouped by offset; operators built on the device
@@ -1489,6 +1498,7 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     cudaGetLastError();
     return f.s;
   } catch (const std::bad_alloc&) {
+    if (getenv("FDA_DEBUG")) fprintf(stderr, "fda: host allocation failed in the plan upload\n");
     free_plan(P.get());
     return FDA_ERR_OOM;
   }

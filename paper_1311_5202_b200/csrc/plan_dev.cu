@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // plan_dev.cu -- device builders of the translation operators.  See plan_dev.cuh.
 #include "plan_dev.cuh"
 
@@ -320,11 +322,19 @@ cudaError_t launch_opjob(const OpJob& J, int pass, cudaStream_t st) {
   grid = std::max<int64_t>(1, std::min<int64_t>(grid, (int64_t)((4ull << 30) / (per * sizeof(double2)))));
   double2* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, (size_t)grid * per * sizeof(double2), st);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    if (getenv("FDA_DEBUG"))
+      fprintf(stderr, "fda: k_opjob workspace of %zu B failed (maxn %d maxs %d)\n", (size_t)grid * per * sizeof(double2),
+              J.maxn, J.maxs);
+    return e;
+  }
   const size_t smem = (size_t)J.maxs * (2 * sizeof(double) + 2 * sizeof(int) + 1) + 16;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_opjob, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_opjob<<<(unsigned)grid, OP_T, smem, st>>>(J, pass, ws, per);
   e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("FDA_DEBUG"))
+    fprintf(stderr, "fda: k_opjob pass %d launch failed (%s): items %d grid %lld smem %zu maxn %d maxs %d ws %zu B\n", pass,
+            cudaGetErrorString(e), J.n_items, (long long)grid, smem, J.maxn, J.maxs, (size_t)grid * per * sizeof(double2));
   cudaFreeAsync(ws, st);
   return e;
 }

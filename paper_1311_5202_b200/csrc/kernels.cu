@@ -2,6 +2,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -894,7 +895,19 @@ static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
   const int cand[6][3] = {{32, 1, 1}, {32, 2, 0}, {32, 1, 0}, {16, 1, 1}, {16, 2, 0}, {16, 1, 0}};
   static const size_t budget = getenv("FDA_GT_SMEM_KB") ? (size_t)atoi(getenv("FDA_GT_SMEM_KB")) * 1024
                                                          : (size_t)GT_SMEM_BUDGET;
+  // FDA_GT_CFG=p,nbuf,stage (experiments): the first candidate at or after it in this list
+  static const int force = [] {
+    const char* f = getenv("FDA_GT_CFG");
+    int a = 0, b = 0, c = 0;
+    if (!f || sscanf(f, "%d,%d,%d", &a, &b, &c) != 3) return -1;
+    const int cl[6][3] = {{32, 1, 1}, {32, 2, 0}, {32, 1, 0}, {16, 1, 1}, {16, 2, 0}, {16, 1, 0}};
+    for (int i = 0; i < 6; ++i)
+      if (cl[i][0] == a && cl[i][1] == b && cl[i][2] == c) return i;
+    return -1;
+  }();
+  int ci = 0;
   for (auto& c : cand) {
+    if (ci++ < force) continue;
     if (c[2] && !allow) continue;
     if (gt_smem(T, c[0], c[1], c[2]) <= budget) {
       *p = c[0], *nbuf = c[1], *stage = c[2];

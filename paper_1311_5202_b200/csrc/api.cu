@@ -1053,6 +1053,14 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     }
     // FDA_M2L_WIN=W (experiment): the LF levels' items end at W Morton windows of target cubes (L2 residency of Y)
     const int win = (!L.hf && getenv("FDA_M2L_WIN")) ? atoi(getenv("FDA_M2L_WIN")) : 0;
+    if (H.opt.verbose) {
+      std::map<int, int64_t> hist;  // pad8 rank -> pairs
+      for (size_t g = 0; g < G.rank.size(); ++g) hist[G.rank[g] < 0 ? -1 : pad8(G.rank[g])] += G.gptr[g + 1] - G.gptr[g];
+      std::ostringstream os;
+      os << "m2l L" << l << " (s " << L.s << ", split at rank " << rlim << "): pairs by pad8 rank:";
+      for (const auto& kv : hist) os << " " << kv.first << ":" << kv.second;
+      H.log += os.str() + "\n";
+    }
     if (!G1.rank.empty() && !G2.rank.empty()) {
       P->lv[l].m2l = make_items(P, G1, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode, win);
       P->lv[l].m2l2 = make_items(P, G2, L.in_cube, L.in_dir, (int64_t)L.cubes.size(), L.s, L.s, raw, dpool, m2l_mode, win);

@@ -28,12 +28,11 @@ __device__ __forceinline__ void cp_async16_w(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 
-constexpr int MW_T = 256;  // threads per CTA (8 warps)
 
 // One task: the (up to) 8 pairs [p0, pe) of a group whose V has RT row tiles (pad8(r) = 8 RT).
 //   Ms: the staged operator; kin: k tiles per row tile of V (level s_in); kt1: k tiles of the group's own
 //   input length; mo: row tiles of the group's own output length; kt2: k tiles of U holding the rank r.
-template <int RT, int NS, int SEC, int MW_D>
+template <int RT, int NS, int MW_D>
 __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin, int kt1, int mo, int kt2, int s_in,
                                          int s_out, int so_own, const double2* __restrict__ X, double2* __restrict__ Y,
                                          const int32_t* __restrict__ pin, const int32_t* __restrict__ pout,
@@ -53,11 +52,9 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
         : "+d"(v.x), "+d"(v.y)
         : "r"((int)(in_slot >= 0 && kt < kt1 && k < s_in)), "l"(xs + k));
   };
-  // output slots: SEC == 0, of the accumulator columns 2t, 2t + 1; SEC == 1, of the columns 2 (lane >> 3) + j
-  // that this lane reduces into in the sector-complete epilogue
-  const int cb = SEC ? 2 * (lane >> 3) : 2 * t;
-  const int o0 = p0 + cb < pe ? pout[p0 + cb] : -1;
-  const int o1 = p0 + cb + 1 < pe ? pout[p0 + cb + 1] : -1;
+  // output slots of the accumulator columns 2t, 2t + 1
+  const int o0 = p0 + 2 * t < pe ? pout[p0 + 2 * t] : -1;
+  const int o1 = p0 + 2 * t + 1 < pe ? pout[p0 + 2 * t + 1] : -1;
 
   double acc[RT][3][2];
 #pragma unroll
@@ -132,48 +129,25 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
       }
     }
     // rows past the group's own output length (a short HF wedge) are exact zeros: no reduction for them
-    if (!SEC) {
-      const int row = mt * 8 + g;
-      if (row < so_own) {
+    const int row = mt * 8 + g;
+    if (row < so_own) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int o = j ? o1 : o0;
-          const double re = c[0][j] - c[1][j], im = c[2][j] - c[0][j] - c[1][j];
-          if (o >= 0) {
-            double2* y = Y + (int64_t)o * s_out + row;
-            atomicAdd(&y->x, re);
-            atomicAdd(&y->y, im);
-          }
+      for (int j = 0; j < 2; ++j) {
+        const int o = j ? o1 : o0;
+        const double re = c[0][j] - c[1][j], im = c[2][j] - c[0][j] - c[1][j];
+        if (o >= 0) {
+          double2* y = Y + (int64_t)o * s_out + row;
+          atomicAdd(&y->x, re);
+          atomicAdd(&y->y, im);
         }
       }
-    } else {
-      // Sector-complete reductions: the L2 applies FP64 reductions per 32-byte sector, and a lane's own values
-      // (re or im of one row, two columns) fill half a sector per instruction.  Shuffled so that lanes 4q..4q+3
-      // add (re, im) of rows 2h, 2h + 1 of one column -- one whole sector (s_out even, so every row pair starts a
-      // sector): 4 instructions per row tile touch 32 sectors instead of 64.  Instruction (j, half): column
-      // 2 (lane >> 3) + j, row pair h = 2 half + ((lane >> 2) & 1), element e = lane & 3 (re/im of row 2h + e/2).
-      double re[2], im[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) re[j] = c[0][j] - c[1][j], im[j] = c[2][j] - c[0][j] - c[1][j];
-      const int e = lane & 3, tq = lane >> 3, hh = (lane >> 2) & 1;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int h = 2 * half + hh, rr = 2 * h + (e >> 1);
-          const int src = rr * 4 + tq;
-          const double vr = __shfl_sync(0xffffffffu, re[j], src), vi = __shfl_sync(0xffffffffu, im[j], src);
-          const int o = j ? o1 : o0, row = mt * 8 + rr;
-          if (o >= 0 && row < so_own)
-            atomicAdd(reinterpret_cast<double*>(Y + (int64_t)o * s_out + row) + (e & 1), (e & 1) ? vi : vr);
-        }
     }
   }
 }
 
 // NS: doubles per staged operator tile (64, or 96 with the 3M sums); RTMAX: largest V row-tile count of the
 // launch's groups; MINB: CTAs per SM the registers are budgeted for
-template <int NS, int RTMAX, int MINB, int SEC>
+template <int NS, int RTMAX, int MINB, int MW_T>
 __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2* __restrict__ X,
                                                          double2* __restrict__ Y) {
   extern __shared__ double msm[];
@@ -210,13 +184,15 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
     for (int64_t task = warp; task < ntask; task += MW_T / 32) {
       const int64_t p0 = pb + 8 * task;
       if (rt == 1 || RTMAX == 1)
-        m2l_task<1, NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<1, NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 2 || RTMAX == 2)
-        m2l_task<(RTMAX >= 2 ? 2 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 2 ? 2 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 3 || RTMAX == 3)
-        m2l_task<(RTMAX >= 3 ? 3 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 3 ? 3 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+      else if (rt == 4 || RTMAX == 4)
+        m2l_task<(RTMAX >= 4 ? 4 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else
-        m2l_task<(RTMAX >= 4 ? 4 : 1), NS, SEC, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        m2l_task<(RTMAX >= 5 ? 5 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
     }
   }
 }
@@ -226,11 +202,11 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
 // read at plan creation (tests toggle it between plans)
 bool m2l_warp_on() { return !(getenv("FDA_M2L_WARP") && getenv("FDA_M2L_WARP")[0] == '0'); }
 
-// largest pad8 rank (<= 32, RT <= 4) whose operator fits smem_limit bytes
+// largest pad8 rank (<= 40, RT <= 5) whose operator fits smem_limit bytes
 int m2l_warp_rmax(int s_out, int s_in, size_t smem_limit) {
   const int kin = (s_in + 3) / 4, mout = (s_out + 7) / 8;
   int best = 0;
-  for (int r8 = 8; r8 <= 32; r8 += 8) {
+  for (int r8 = 8; r8 <= 40; r8 += 8) {
     const int rt = r8 / 8;
     if ((size_t)(rt * kin + mout * 2 * rt) * 64 * sizeof(double) <= smem_limit) best = r8;
   }
@@ -238,35 +214,32 @@ int m2l_warp_rmax(int s_out, int s_in, size_t smem_limit) {
 }
 
 bool m2l_warp_fits(const GTrans& T) {
-  return T.warp_tasks && T.atomic && T.all_lowrank && T.rmax8 <= 32 && (size_t)T.mmax * sizeof(double) <= smem_optin_bytes();
+  return T.warp_tasks && T.atomic && T.all_lowrank && T.rmax8 <= 40 && (size_t)T.mmax * sizeof(double) <= smem_optin_bytes();
 }
 
 cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaStream_t st) {
   if (T.n_items <= 0) return cudaSuccess;
   // Configuration: three CTAs per SM (24 warps: more latency hiding; registers budgeted for RTMAX <= 2) when the
-  // operator fits a third of the shared memory, else two; the tiles carry the 3M sums when those still fit
-  // (FDA_M2L_SUM3=0: never; FDA_M2L_OCC=2: at most two CTAs per SM)
+  // operator fits a third of the shared memory, else two of 8 warps; operators larger than half the shared memory
+  // (the high ranks of the LF level) run as one CTA of 16 warps per SM.  The tiles carry the 3M sums when those
+  // still fit (FDA_M2L_SUM3=0: never; FDA_M2L_OCC=2: at most two CTAs per SM)
   const size_t sm2 = (size_t)T.mmax * sizeof(double), sm3 = sm2 * 3 / 2;
   const size_t third = 74 * 1024;
+  const bool big = sm2 > (size_t)GT_SMEM_BUDGET;
   const bool allow3 = !(getenv("FDA_M2L_SUM3") && getenv("FDA_M2L_SUM3")[0] == '0');
-  const bool occ3 = T.rmax8 <= 16 && sm2 <= third && !(getenv("FDA_M2L_OCC") && getenv("FDA_M2L_OCC")[0] == '2');
-  const bool sum3 = allow3 && sm3 <= (occ3 ? third : (size_t)GT_SMEM_BUDGET);
+  const bool occ3 =
+      !big && T.rmax8 <= 16 && sm2 <= third && !(getenv("FDA_M2L_OCC") && getenv("FDA_M2L_OCC")[0] == '2');
+  const bool sum3 = allow3 && sm3 <= (big ? smem_optin_bytes() : occ3 ? third : (size_t)GT_SMEM_BUDGET);
   const size_t sm = sum3 ? sm3 : sm2;
-  // sector-complete reductions on the launches the plan marked (none by default: measured at config 5, M2L
-  // 162.8 ms with them on the LF level against 158.2 without, profiles/r02/ab_c5.log); they need an even s_out.
-  // FDA_M2L_SECTOR=0 / 2: never / on every level
-  const char* se = getenv("FDA_M2L_SECTOR");
-  const bool sec = T.s_out % 2 == 0 && (se ? se[0] == '2' || (se[0] != '0' && T.sector) : T.sector);
   void (*kern)(GTrans, const double2*, double2*) =
-      sec ? (occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 1> : k_m2l_warp<64, 2, 3, 1>)
-                  : (sum3 ? k_m2l_warp<96, 4, 2, 1> : k_m2l_warp<64, 4, 2, 1>))
-          : (occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 0> : k_m2l_warp<64, 2, 3, 0>)
-                  : (sum3 ? k_m2l_warp<96, 4, 2, 0> : k_m2l_warp<64, 4, 2, 0>));
+      big ? (sum3 ? k_m2l_warp<96, 5, 1, 512> : k_m2l_warp<64, 5, 1, 512>)
+          : occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 256> : k_m2l_warp<64, 2, 3, 256>)
+                 : (sum3 ? k_m2l_warp<96, 4, 2, 256> : k_m2l_warp<64, 4, 2, 256>);
   if (sm > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  kern<<<(unsigned)T.n_items, MW_T, sm, st>>>(T, X, Y);
+  kern<<<(unsigned)T.n_items, big ? 512 : 256, sm, st>>>(T, X, Y);
   return cudaGetLastError();
 }
 

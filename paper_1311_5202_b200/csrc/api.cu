@@ -1672,8 +1672,14 @@ void stage_up(fda_plan P, uint32_t mask, double2* sendbuf, cudaStream_t st, Mark
 void stage_near(fda_plan P, uint32_t mask, cudaStream_t st, Marks& mk) {
   const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
   mk.begin(1);
-  if (!(mask & FDA_PHASE_NEAR) || partial) ck(cudaMemsetAsync(P->outm, 0, (size_t)P->n * sizeof(double2), st));
-  if (mask & FDA_PHASE_NEAR)
+  // symmetric P2P (each leaf pair once, both directions; BM_H on a single-rank plan; FDA_P2P_SYM=0: off)
+  const bool sym = (mask & FDA_PHASE_NEAR) && !partial && P->kind == 0 &&
+                   !(getenv("FDA_P2P_SYM") && getenv("FDA_P2P_SYM")[0] == '0');
+  if (!(mask & FDA_PHASE_NEAR) || partial || sym) ck(cudaMemsetAsync(P->outm, 0, (size_t)P->n * sizeof(double2), st));
+  if (sym)
+    fda::launch_p2p_sym(P->nleaf, P->leaf_ptr, P->p2p_ptr, P->p2p_src, points_of(P), P->q, P->H.k, alpha_of(P),
+                        P->outm, st);
+  else if (mask & FDA_PHASE_NEAR)
     fda::launch_p2p(P->kind, P->leaf_e - P->leaf_b, P->leaf_ptr, P->p2p_ptr, P->p2p_src, points_of(P), P->q, P->H.k,
                     alpha_of(P), P->outm, P->leaf_b, st);
   mk.end(1);

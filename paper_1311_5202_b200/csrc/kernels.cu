@@ -245,6 +245,148 @@ __global__ void __launch_bounds__(P2P_T) k_p2p(const int64_t* __restrict__ leaf_
     __syncthreads();
   }
 }
+// Symmetric P2P for the BM_H kernel (single-rank plans): the near-field list is symmetric (leaf pair (T, S) is
+// P2P iff (S, T) is, R20), and K_ij, K_ji share r, e^{ikr} and the alpha term: with d = x_i - x_j,
+// a = d.n_i, b = d.n_j, c = n_i.n_j, E = e^{ikr}/(4 pi), u = ikr - 1,
+//   C    = alpha ((3 - 3ikr - k^2 r^2) a b / r^5 + u c / r^3)
+//   K_ij = -E (u b / r^3 + C),   K_ji = -E (-u a / r^3 + C)          (eq_hmat)
+// The CTA of leaf T takes the pairs with source leaves S > T in both directions (the source side is reduced
+// over the targets of the warp segment by shuffles, then one FP64 reduction per source point) and its own
+// leaf S = T one way (j != i); outputs accumulate with FP64 reductions into the zeroed outm.
+__device__ __forceinline__ void bm_h_pair(double dx, double dy, double dz, double nxx, double nxy, double nxz,
+                                          double nyx, double nyy, double nyz, double k, double2 alpha, double2& kij,
+                                          double2& kji) {
+  const double r2 = dx * dx + dy * dy + dz * dz;
+  const double ir = rsqrt(r2);
+  const double r = r2 * ir;
+  const double kr = k * r;
+  double sn, cs;
+  sincos(kr, &sn, &cs);
+  const double a = dx * nxx + dy * nxy + dz * nxz;
+  const double b = dx * nyx + dy * nyy + dz * nyz;
+  const double c = nxx * nyx + nxy * nyy + nxz * nyz;
+  const double ir2 = ir * ir;
+  const double2 u = make_double2(-1.0, kr);
+  const double2 v = make_double2(3.0 - kr * kr, -3.0 * kr);
+  // alpha (v a b / r^2 + u c)  (the common 1/r^3 is in f)
+  double2 w = make_double2(u.x * c, u.y * c);
+  const double ab = a * b * ir2;
+  w.x = fma(v.x, ab, w.x);
+  w.y = fma(v.y, ab, w.y);
+  const double2 C = cmul(alpha, w);
+  const double f = -FDA_INV4PI * ir2 * ir;  // -1/(4 pi r^3)
+  const double2 E = make_double2(cs * f, sn * f);
+  kij = cmul(E, make_double2(fma(u.x, b, C.x), fma(u.y, b, C.y)));
+  kji = cmul(E, make_double2(fma(-u.x, a, C.x), fma(-u.y, a, C.y)));
+}
+
+__global__ void __launch_bounds__(P2P_T) k_p2p_sym(const int64_t* __restrict__ leaf_ptr,
+                                                   const int64_t* __restrict__ p2p_ptr,
+                                                   const int32_t* __restrict__ p2p_src, Points P,
+                                                   const double2* __restrict__ q, double k, double2 alpha,
+                                                   double2* __restrict__ outm) {
+  __shared__ double sx[P2P_T], sy[P2P_T], sz[P2P_T], snx[P2P_T], sny[P2P_T], snz[P2P_T];
+  __shared__ double2 sq[P2P_T];
+  __shared__ int64_t sj[P2P_T];
+  __shared__ int64_t lpre[P2P_MAXL + 1], lbeg[P2P_MAXL];
+  __shared__ int lself[P2P_MAXL];
+  __shared__ char sself[P2P_T];
+  __shared__ double2 red[P2P_T];
+  const int64_t t = blockIdx.x;
+  const int64_t tb = leaf_ptr[t], te = leaf_ptr[t + 1];
+  const int nt = (int)(te - tb);
+  const int ntp = nt >= 32 ? 32 : next_pow2(nt);  // targets per segment: a power of two within one warp
+  const int nsl = P2P_T / ntp;
+  const int my_t = threadIdx.x % ntp, my_sl = threadIdx.x / ntp;
+  const int64_t sb0 = p2p_ptr[t], se0 = p2p_ptr[t + 1];
+  for (int t0 = 0; t0 < nt; t0 += ntp) {
+    const int64_t i = tb + t0 + my_t;
+    const bool act = (t0 + my_t) < nt;
+    double xi = 0, yi = 0, zi = 0, nxi = 0, nyi = 0, nzi = 0;
+    double2 qi = make_double2(0.0, 0.0);
+    if (act) xi = P.x[i], yi = P.y[i], zi = P.z[i], nxi = P.nx[i], nyi = P.ny[i], nzi = P.nz[i], qi = q[i];
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t sb = sb0; sb < se0; sb += P2P_MAXL) {
+      const int nl = (int)min((int64_t)P2P_MAXL, se0 - sb);
+      __syncthreads();
+      for (int l = threadIdx.x; l < nl; l += P2P_T) {
+        const int64_t s = p2p_src[sb + l];
+        lbeg[l] = leaf_ptr[s];
+        lpre[l + 1] = s >= t ? leaf_ptr[s + 1] - leaf_ptr[s] : 0;  // source leaves S >= T only
+        lself[l] = s == t;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        lpre[0] = 0;
+        for (int l = 0; l < nl; ++l) lpre[l + 1] += lpre[l];
+      }
+      __syncthreads();
+      const int64_t tot = lpre[nl];
+      for (int64_t s0 = 0; s0 < tot; s0 += P2P_T) {
+        const int64_t jj = s0 + threadIdx.x;
+        if (jj < tot) {
+          int lo = 0, hi = nl - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (lpre[mid] <= jj) lo = mid;
+            else hi = mid - 1;
+          }
+          const int64_t j = lbeg[lo] + (jj - lpre[lo]);
+          sx[threadIdx.x] = P.x[j], sy[threadIdx.x] = P.y[j], sz[threadIdx.x] = P.z[j];
+          snx[threadIdx.x] = P.nx[j], sny[threadIdx.x] = P.ny[j], snz[threadIdx.x] = P.nz[j];
+          sq[threadIdx.x] = q[j];
+          sj[threadIdx.x] = j;
+          sself[threadIdx.x] = (char)lself[lo];
+        }
+        __syncthreads();
+        const int cnt = (int)min((int64_t)P2P_T, tot - s0);
+        // uniform trip count over the slices of a warp (the source-side reduction shuffles need every lane)
+        for (int m = 0; m * nsl < cnt; ++m) {
+          const int u = m * nsl + my_sl;
+          const bool on = u < cnt;
+          double2 kij = make_double2(0.0, 0.0), kji = kij;
+          bool self = false;
+          if (on) {
+            self = sself[u] != 0;
+            if (act && sj[u] != i)
+              bm_h_pair(xi - sx[u], yi - sy[u], zi - sz[u], nxi, nyi, nzi, snx[u], sny[u], snz[u], k, alpha, kij,
+                        kji);
+            cfma(acc, kij, sq[u]);
+          }
+          // source side (S > T): sum over this segment's targets of K_ji q_i, one reduction per source point
+          double2 v = make_double2(0.0, 0.0);
+          if (on && !self) cfma(v, kji, qi);
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1)
+            if (o < ntp) {
+              v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+              v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+            }
+          if (on && !self && my_t == 0) {
+            atomicAdd(&outm[sj[u]].x, v.x);
+            atomicAdd(&outm[sj[u]].y, v.y);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (my_sl == 0 && act) {
+      double2 s = red[my_t];
+      for (int sl = 1; sl < nsl; ++sl) s = cadd(s, red[my_t + sl * ntp]);
+      atomicAdd(&outm[i].x, s.x);
+      atomicAdd(&outm[i].y, s.y);
+    }
+    __syncthreads();
+  }
+}
+void launch_p2p_sym(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src, Points P,
+                    const double2* q, double k, double2 alpha, double2* outm, cudaStream_t st) {
+  if (nleaf <= 0) return;
+  k_p2p_sym<<<(unsigned)nleaf, P2P_T, 0, st>>>(leaf_ptr, p2p_ptr, p2p_src, P, q, k, alpha, outm);
+}
+
 void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
                 Points P, const double2* q, double k, double2 alpha, double2* outm, int64_t leaf0, cudaStream_t st) {
   if (nleaf <= 0) return;

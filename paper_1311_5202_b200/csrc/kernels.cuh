@@ -37,6 +37,9 @@ void launch_xunpack(int64_t ndst, const int64_t* xoff, const int32_t* len, const
 void launch_p2p(int kind, int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src,
                 Points P, const double2* q, double k, double2 alpha, double2* outm, int64_t tgt_leaf_begin,
                 cudaStream_t st);
+// symmetric P2P of the BM_H kernel over the whole plan (single rank): outm must be zeroed first (FP64 reductions)
+void launch_p2p_sym(int64_t nleaf, const int64_t* leaf_ptr, const int64_t* p2p_ptr, const int32_t* p2p_src, Points P,
+                    const double2* q, double k, double2 alpha, double2* outm, cudaStream_t st);
 void launch_csr(int64_t row_begin, int64_t row_end, const int64_t* rp, const int32_t* col, const double2* val,
                 const double2* phim, double2* outm, cudaStream_t st);
 // H4: check potentials chk[t][i] of leaf leaf_ids[t] on its check surface (nsurf points, relative):

@@ -160,3 +160,33 @@ def test_full_apply_full_oracle(name, nu, k, opts):
     far_err = oracle.rel_l2(got - near, ref - near)
     print(f"{name}: N={p.N} rel l2 {err:.3e}  far-only {far_err:.3e}")
     assert err <= 1e-4
+
+
+@pytest.mark.parametrize("nu,k", [(8, 5.0), (24, 50.0)])
+def test_symmetric_p2p_equals_one_sided_p2p(nu, k):
+    """The symmetric P2P (kernels.cu k_p2p_sym: each leaf pair once, K_ij and K_ji from one evaluation of r and
+    e^{ikr}) against the one-sided kernel (FDA_P2P_SYM=0) and against oracle_near on the plan's leaf pairs."""
+    import os
+    fda = _fda()
+    p = synth.make_problem("x", k=k, nu=nu)
+    phi = synth.random_phi(p.N, 3)
+    h = _plan(p)
+    try:
+        sym = _run(h, phi, fda.FDA_PHASE_NEAR)
+        os.environ["FDA_P2P_SYM"] = "0"
+        try:
+            one = _run(h, phi, fda.FDA_PHASE_NEAR)
+        finally:
+            del os.environ["FDA_P2P_SYM"]
+        lop, lev, ijk = fda.fda_plan_export_leaves(h, p.N)
+        t, s = fda.fda_plan_export_p2p(h)
+    finally:
+        fda.fda_plan_destroy(h)
+    err = oracle.rel_l2(sym, one)
+    order = np.argsort(lop, kind="stable")
+    leaf_ptr = np.concatenate([[0], np.cumsum(np.bincount(lop, minlength=lev.shape[0]))])
+    pair_ptr = np.concatenate([[0], np.cumsum(np.bincount(t, minlength=lev.shape[0]))])
+    ref = oracle.apply_near(p.x, p.n, p.w, p.k, p.alpha, phi, leaf_ptr, order, pair_ptr, s)
+    print(f"N={p.N}: symmetric vs one-sided P2P {err:.3e}, vs oracle_near {oracle.rel_l2(sym, ref):.3e}")
+    assert err <= 1e-13
+    assert oracle.rel_l2(sym, ref) <= 1e-12

@@ -98,7 +98,8 @@ typedef struct {
   int32_t rank, nranks;    /* multi-GPU: this rank owns the rank-th of nranks Morton ranges of leaves (default 0/1);
                               nranks <= 64; see fda_plan_create_dist / fda_apply_up */
   int32_t verbose;         /* plan log (fda_plan_log) */
-  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps / 3 (R23) */
+  double eps_lowrank;      /* low-rank M2L truncation sigma_i < eps_lowrank sigma_1; 0 -> eps, 10x tighter
+                              on the low-frequency LF levels (R23) */
   int32_t kernel;          /* FDA_KERNEL_BMH (default): K = dG/dn_y + alpha d2G/dn_x dn_y (eq_hmat);
                               FDA_KERNEL_BMG: K = G + alpha dG/dn_x (eq_gmat);
                               FDA_KERNEL_T1: K = G + alpha dG/dn_y (eq_sum; Table 1 mode,

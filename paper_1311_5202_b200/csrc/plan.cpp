@@ -184,7 +184,11 @@ std::string build_plan(HostPlan& P, int64_t n, const double* x, const double* nr
   // DESIGN.md R11 / R23: expansion truncation (R+, HF interpolative selection) at eps_int, low-rank M2L
   // truncation at eps_lr (measured: the low-rank cut contributes no visible error at eps_int)
   P.eps_int = opt.eps_int > 0 ? opt.eps_int : eps / 100.0;
-  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / 3.0;
+  // the paper's cut, sigma_i < eps sigma_1 dropped; measured at config 5 (profiles/r02/
+  // epslr_c5.log): M2L 137.9 ms, parity 2.2e-5 (far-only 2.8e-4) against 144.7 ms, 1.8e-5 (2.3e-4) with eps / 3.
+  // FDA_EPS_LR_DIV=d (experiments): eps_lr = eps / d
+  const double lr_div = getenv("FDA_EPS_LR_DIV") ? std::max(0.1, atof(getenv("FDA_EPS_LR_DIV"))) : 1.0;
+  P.eps_lr = opt.eps_lr > 0 ? opt.eps_lr : eps / lr_div;
   // N_p = max(30, 50(-log10 eps - 3))  (eq_npleaf, sign-corrected; R12)
   P.np = leaf_size_for(eps, opt.np);
   const double lambda = k > 0 ? 2.0 * PI / k : INFINITY;

@@ -24,7 +24,7 @@ namespace fda {
 struct Options {
   int np = 0;               // leaf threshold N_p; 0 -> from eps (eq_npleaf, sign-corrected)
   double eps_int = 0;       // expansion truncation tolerance; 0 -> eps / 100 (R11)
-  double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps / 3 (R23)
+  double eps_lr = 0;        // low-rank M2L truncation tolerance; 0 -> eps (R23)
   int lf_p_low = 0;         // LF surface points per edge for w/lambda < lf_p_switch; 0 -> 6 + dp(eps)
   int lf_p_high = 0;        // ... for w/lambda >= lf_p_switch; 0 -> 8 + dp(eps)  (R17)
   double lf_p_switch = 0.75;

@@ -127,6 +127,8 @@ typedef struct {
   int64_t xchg_send_bytes, xchg_recv_bytes;   /* multi-GPU: expansion bytes this rank sends / receives per apply */
   int64_t m2l_ops;  /* distinct M2L operators stored: (offset, wedge) groups related by a cube symmetry share one
                        (the wedges' point sets are rotations of one set), m2l_ops <= m2l_groups */
+  double bytes_s2m, bytes_l2t;  /* algorithmic bytes per apply of the stored leaf S2M / L2T matrices (PAPER.md:979-980:
+                                   "precomputed and saved in memory"); 0 when the kernels are evaluated on the fly */
 } fda_stats;
 
 void fda_options_default(fda_options* opt);

@@ -54,6 +54,11 @@ struct DevLeafOps {
   double* surf = nullptr;
   fda::GTrans s2m;           // H4 reduction: X[slot] += S chk[t]            (S = Sigma^-1 U^H, eq_cmps)
   fda::GTrans l2t;           // H8 reduction: rho[t'] += T Y[slot]           (T = conj(U) Sigma^-1, eq_cmpt)
+  // stored leaf matrices (kernels.cuh launch_leafmat), null when not stored
+  int64_t* pofs = nullptr;   // owned leaf t -> first row (point) of its matrices
+  int32_t* slot = nullptr;   // owned leaf t -> its out (= in) slot
+  double2* Sm = nullptr;     // rows per source point: S_leaf = Sigma^-1 U^H E_up
+  double2* Tm = nullptr;     // rows per target point: T_leaf = E_dn conj(U) Sigma^-1
 };
 
 }  // namespace
@@ -294,6 +299,10 @@ std::vector<int32_t> m2l_symmetry_classes(const fda::Level& L, const fda::HostPl
   }
   return cls;
 }
+
+fda::Points points_of(fda_plan P);
+fda::LeafGeom leaves_of(fda_plan P);
+double2 alpha_of(fda_plan P);
 
 // Work items of a grouped translation.  raw != nullptr: the groups' matrices are the host column-major pool
 // raw (G.mat offsets), converted to fragment order and uploaded; raw == nullptr: they are already in the
@@ -1212,13 +1221,51 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       G.mat.push_back(0);
       D.l2t = make_items(P, G, oc, od, (int64_t)L.cubes.size(), L.nsurf, L.s, O.T.data());
     }
-    P->surfbuf_n = std::max(P->surfbuf_n, (int64_t)lo_.size() * L.nsurf);
-    for (size_t t = 0; t < lo_.size(); ++t) {
-      const int64_t npt = lp[lo_[t] + 1] - lp[lo_[t]];
-      P->st.s2m_evals += npt * L.nsurf;
-      P->st.l2t_evals += npt * L.nsurf;
-      P->st.flops_s2m += 8.0 * L.s * L.nsurf;  // the reduction x~ = S chk (eq_cmps); the evaluations are counted apart
-      P->st.flops_l2t += 8.0 * L.s * L.nsurf;
+    // "In the FDBEM, the S2M and L2T matrices are precomputed and saved in memory": the
+    // per-leaf matrices S_leaf (s x n) and T_leaf (n x s) are built here once when they take <= 40% of the free
+    // device memory (FDA_LEAF_MATS=0: never; then the apply evaluates the kernels on the surfaces every time)
+    std::vector<int64_t> pofs(lo_.size() + 1, 0);
+    for (size_t t = 0; t < lo_.size(); ++t) pofs[t + 1] = pofs[t] + (lp[lo_[t] + 1] - lp[lo_[t]]);
+    const double mat_bytes = 2.0 * (double)pofs.back() * L.s * sizeof(double2);
+    bool mats = !(getenv("FDA_LEAF_MATS") && getenv("FDA_LEAF_MATS")[0] == '0');
+    if (mats) {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError(), fr = 0;
+      mats = mat_bytes <= 0.4 * (double)fr;
+    }
+    if (mats) {
+      D.pofs = upload(P, pofs);
+      std::vector<int32_t> sl(so_.begin(), so_.end());
+      D.slot = upload(P, sl);
+      D.Sm = dalloc<double2>(P, (size_t)pofs.back() * L.s);
+      D.Tm = dalloc<double2>(P, (size_t)pofs.back() * L.s);
+      std::vector<double> sred(2 * O.S.size()), tredt(2 * O.T.size());
+      for (size_t i = 0; i < O.S.size(); ++i) sred[2 * i] = O.S[i].real(), sred[2 * i + 1] = O.S[i].imag();
+      for (int b = 0; b < L.nsurf; ++b)  // O.T: nsurf x s column-major -> row-major
+        for (int c = 0; c < L.s; ++c) {
+          const cplx v = O.T[b + (size_t)c * L.nsurf];
+          tredt[2 * ((size_t)b * L.s + c)] = v.real(), tredt[2 * ((size_t)b * L.s + c) + 1] = v.imag();
+        }
+      const double* d_sred = upload(P, sred);
+      const double* d_tredt = upload(P, tredt);
+      const double2 alpha_dn = P->kind == FDA_KERNEL_T1 ? make_double2(0.0, 0.0) : alpha_of(P);
+      fda::launch_leafmat(P->kind, (int64_t)lo_.size(), D.leaf_own, D.pofs, leaves_of(P), points_of(P), D.surf,
+                          L.nsurf, H.k, alpha_of(P), alpha_dn, reinterpret_cast<const double2*>(d_sred),
+                          reinterpret_cast<const double2*>(d_tredt), L.s, D.Sm, D.Tm, 0);
+      ck(cudaGetLastError());
+      P->st.bytes_s2m += (double)pofs.back() * L.s * sizeof(double2);
+      P->st.bytes_l2t += (double)pofs.back() * L.s * sizeof(double2);
+      P->st.flops_s2m += 8.0 * (double)pofs.back() * L.s;  // x~ = S_leaf q
+      P->st.flops_l2t += 8.0 * (double)pofs.back() * L.s;
+    } else {
+      P->surfbuf_n = std::max(P->surfbuf_n, (int64_t)lo_.size() * L.nsurf);
+      for (size_t t = 0; t < lo_.size(); ++t) {
+        const int64_t npt = lp[lo_[t] + 1] - lp[lo_[t]];
+        P->st.s2m_evals += npt * L.nsurf;
+        P->st.l2t_evals += npt * L.nsurf;
+        P->st.flops_s2m += 8.0 * L.s * L.nsurf;  // the reduction x~ = S chk (eq_cmps); the evaluations are counted apart
+        P->st.flops_l2t += 8.0 * L.s * L.nsurf;
+      }
     }
     P->lo.push_back(D);
   }
@@ -1651,9 +1698,14 @@ void stage_up(fda_plan P, uint32_t mask, double2* sendbuf, cudaStream_t st, Mark
   // M2M accumulates into the non-leaf slots: clear every level's outgoing expansions first
   if (P->xoff.back()) ck(cudaMemsetAsync(P->Xall, 0, (size_t)P->xoff.back() * sizeof(double2), st));
   for (const auto& O : P->lo) {
-    fda::launch_s2m_check(P->kind, O.nleaves_own, O.leaf_own, Lg, Pt, P->q, O.surf, O.nsurf, P->H.k, alpha_of(P),
-                          P->surfbuf, st);
-    ck(fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st));
+    if (O.Sm) {  // stored S_leaf
+      fda::launch_leaf_s2m(O.nleaves_own, O.leaf_own, O.pofs, O.slot, P->leaf_ptr, P->q, O.Sm, O.s, P->lv[O.level].X,
+                           st);
+    } else {
+      fda::launch_s2m_check(P->kind, O.nleaves_own, O.leaf_own, Lg, Pt, P->q, O.surf, O.nsurf, P->H.k, alpha_of(P),
+                            P->surfbuf, st);
+      ck(fda::launch_gtrans(O.s2m, P->surfbuf, P->lv[O.level].X, st));
+    }
     tr(st, "s2m", O.level);
   }
   mk.end(3);
@@ -1722,6 +1774,12 @@ void stage_down(fda_plan P, uint32_t mask, const double2* recvbuf, cudaStream_t 
   mk.begin(7);
   if (near_done) ck(cudaStreamWaitEvent(st, near_done, 0));  // L2T adds into the rows P2P / CSR wrote
   for (const auto& O : P->lo) {
+    if (O.Tm) {  // stored T_leaf
+      fda::launch_leaf_l2t(O.nleaves_own, O.leaf_own, O.pofs, O.slot, P->leaf_ptr, P->lv[O.level].Y, O.Tm, O.s,
+                           P->outm, st);
+      tr(st, "l2t", O.level);
+      continue;
+    }
     ck(cudaMemsetAsync(P->surfbuf, 0, (size_t)O.nleaves_own * O.nsurf * sizeof(double2), st));
     ck(fda::launch_gtrans(O.l2t, P->lv[O.level].Y, P->surfbuf, st));
     // E_dn = G + alpha dG/dn_x (BM_H, BM_G: PAPER.md eq_eval2t); the Table-1 kernel has no target
@@ -1739,7 +1797,7 @@ int64_t count_launches(fda_plan P, uint32_t mask) {
   int64_t L = 3;  // permute, p2p, unpermute
   if ((mask & FDA_PHASE_CORR) && P->nnz > 0) ++L;
   if (has_far(P, mask)) {
-    for (const auto& O : P->lo) L += 4 * (O.nleaves_own > 0);
+    for (const auto& O : P->lo) L += (O.Sm ? 2 : 4) * (O.nleaves_own > 0);
     for (const auto& T : P->tr) L += (T.up.n_items > 0) + (T.dn.n_items > 0);
     for (const auto& D : P->lv) L += (D.m2l.n_items > 0) + (D.m2l2.n_items > 0) + 2 * (D.m2lb.n_blocks > 0);
     if (P->nranks > 1) L += (P->xc.nsend > 0) + (P->xc.ndst > 0);

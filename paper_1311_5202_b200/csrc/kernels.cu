@@ -1193,6 +1193,127 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
   return gt_launch<8, 1, false>(T, X, Y, sm, st);
 }
 
+// ---------------------------------------------------------------- stored leaf S2M / L2T matrices
+// "In the FDBEM, the S2M and L2T matrices are precomputed and saved in memory": per leaf,
+//   S_leaf = (Sigma^-1 U^H) E_up  (s x n_leaf; eq_cmps x eq_evas2mh)   rows stored per source point: Sm[j][c]
+//   T_leaf = E_dn (conj(U) Sigma^-1) (n_leaf x s; eq_eval2t x eq_cmpt) rows stored per target point: Tm[i][c]
+// so the apply's S2M is x~[slot] = S_leaf q_leaf and its L2T out_i += T_leaf[i] y~[slot]: one HBM read of the
+// matrices instead of the kernel evaluations on the check / equivalent surfaces.
+#define LM_T 128
+template <int KIND>
+__global__ void __launch_bounds__(LM_T) k_leafmat_s2m(const int32_t* __restrict__ leaf_ids, const int64_t* __restrict__ pofs,
+                                                      LeafGeom L, Points P, const double* __restrict__ surf, int nsurf,
+                                                      double k, double2 alpha, const double2* __restrict__ Sred, int s,
+                                                      double2* __restrict__ Sm) {
+  extern __shared__ double2 e[];  // nsurf kernel values of one source point
+  const int64_t leaf = leaf_ids[blockIdx.x];
+  const int64_t pb = L.ptr[leaf], pe = L.ptr[leaf + 1];
+  const double cx = L.cx[leaf], cy = L.cy[leaf], cz = L.cz[leaf];
+  for (int64_t j = pb; j < pe; ++j) {
+    const double yx = P.x[j], yy = P.y[j], yz = P.z[j], nyx = P.nx[j], nyy = P.ny[j], nyz = P.nz[j];
+    __syncthreads();
+    for (int a = threadIdx.x; a < nsurf; a += LM_T) {
+      const double ax = cx + surf[3 * a], ay = cy + surf[3 * a + 1], az = cz + surf[3 * a + 2];
+      e[a] = KIND == 0   ? dg_dny(ax - yx, ay - yy, az - yz, nyx, nyy, nyz, k)
+             : KIND == 1 ? g_only(ax - yx, ay - yy, az - yz, k)
+                         : bm_g(ax - yx, ay - yy, az - yz, -nyx, -nyy, -nyz, k, alpha);
+    }
+    __syncthreads();
+    double2* row = Sm + (pofs[blockIdx.x] + (j - pb)) * s;
+    for (int c = threadIdx.x; c < s; c += LM_T) {  // Sred column-major s x nsurf
+      double2 acc = make_double2(0.0, 0.0);
+      for (int a = 0; a < nsurf; ++a) cfma(acc, Sred[c + (int64_t)a * s], e[a]);
+      row[c] = acc;
+    }
+  }
+}
+__global__ void __launch_bounds__(LM_T) k_leafmat_l2t(const int32_t* __restrict__ leaf_ids, const int64_t* __restrict__ pofs,
+                                                      LeafGeom L, Points P, const double* __restrict__ surf, int nsurf,
+                                                      double k, double2 alpha, const double2* __restrict__ TredT, int s,
+                                                      double2* __restrict__ Tm) {
+  extern __shared__ double2 e[];  // nsurf kernel values of one target point
+  const int64_t leaf = leaf_ids[blockIdx.x];
+  const int64_t pb = L.ptr[leaf], pe = L.ptr[leaf + 1];
+  const double cx = L.cx[leaf], cy = L.cy[leaf], cz = L.cz[leaf];
+  for (int64_t i = pb; i < pe; ++i) {
+    const double xi = P.x[i] - cx, yi = P.y[i] - cy, zi = P.z[i] - cz, nxi = P.nx[i], nyi = P.ny[i], nzi = P.nz[i];
+    __syncthreads();
+    for (int b = threadIdx.x; b < nsurf; b += LM_T)
+      e[b] = bm_g(xi - surf[3 * b], yi - surf[3 * b + 1], zi - surf[3 * b + 2], nxi, nyi, nzi, k, alpha);
+    __syncthreads();
+    double2* row = Tm + (pofs[blockIdx.x] + (i - pb)) * s;
+    for (int c = threadIdx.x; c < s; c += LM_T) {  // TredT row-major nsurf x s (the transpose of T's storage)
+      double2 acc = make_double2(0.0, 0.0);
+      for (int b = 0; b < nsurf; ++b) cfma(acc, e[b], TredT[(int64_t)b * s + c]);
+      row[c] = acc;
+    }
+  }
+}
+void launch_leafmat(int kind, int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, LeafGeom L, Points P,
+                    const double* surf, int nsurf, double k, double2 alpha, double2 alpha_dn, const double2* Sred,
+                    const double2* TredT, int s, double2* Sm, double2* Tm, cudaStream_t st) {
+  if (nleaves <= 0) return;
+  const size_t sm = (size_t)nsurf * sizeof(double2);
+  if (kind == 0)
+    k_leafmat_s2m<0><<<(unsigned)nleaves, LM_T, sm, st>>>(leaf_ids, pofs, L, P, surf, nsurf, k, alpha, Sred, s, Sm);
+  else if (kind == 1)
+    k_leafmat_s2m<1><<<(unsigned)nleaves, LM_T, sm, st>>>(leaf_ids, pofs, L, P, surf, nsurf, k, alpha, Sred, s, Sm);
+  else
+    k_leafmat_s2m<2><<<(unsigned)nleaves, LM_T, sm, st>>>(leaf_ids, pofs, L, P, surf, nsurf, k, alpha, Sred, s, Sm);
+  k_leafmat_l2t<<<(unsigned)nleaves, LM_T, sm, st>>>(leaf_ids, pofs, L, P, surf, nsurf, k, alpha_dn, TredT, s, Tm);
+}
+
+// apply: x~[slot] = sum_j Sm[j] q_j (threads over the expansion index; each row read once, coalesced)
+__global__ void __launch_bounds__(LM_T) k_leaf_s2m(const int32_t* __restrict__ leaf_ids, const int64_t* __restrict__ pofs,
+                                                   const int32_t* __restrict__ slot, const int64_t* __restrict__ lptr,
+                                                   const double2* __restrict__ q, const double2* __restrict__ Sm, int s,
+                                                   double2* __restrict__ X) {
+  const int64_t leaf = leaf_ids[blockIdx.x];
+  const int64_t pb = lptr[leaf], pe = lptr[leaf + 1];
+  const double2* rows = Sm + pofs[blockIdx.x] * s;
+  double2* x = X + (int64_t)slot[blockIdx.x] * s;
+  for (int c = threadIdx.x; c < s; c += LM_T) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t j = pb; j < pe; ++j) cfma(acc, __ldg(rows + (j - pb) * s + c), __ldg(q + j));
+    x[c] = acc;
+  }
+}
+// apply: out_i += Tm[i] . y~[slot] (a warp per target point, lanes along the expansion, shuffle reduction)
+__global__ void __launch_bounds__(LM_T) k_leaf_l2t(const int32_t* __restrict__ leaf_ids, const int64_t* __restrict__ pofs,
+                                                   const int32_t* __restrict__ slot, const int64_t* __restrict__ lptr,
+                                                   const double2* __restrict__ Y, const double2* __restrict__ Tm, int s,
+                                                   double2* __restrict__ outm) {
+  extern __shared__ double2 y[];
+  const int64_t leaf = leaf_ids[blockIdx.x];
+  const int64_t pb = lptr[leaf], pe = lptr[leaf + 1];
+  const double2* yl = Y + (int64_t)slot[blockIdx.x] * s;
+  for (int c = threadIdx.x; c < s; c += LM_T) y[c] = yl[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double2* rows = Tm + pofs[blockIdx.x] * s;
+  for (int64_t i = pb + warp; i < pe; i += LM_T / 32) {
+    const double2* r = rows + (i - pb) * s;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int c = lane; c < s; c += 32) cfma(acc, __ldg(r + c), y[c]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) outm[i] = cadd(outm[i], acc);
+  }
+}
+void launch_leaf_s2m(int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, const int32_t* slot,
+                     const int64_t* lptr, const double2* q, const double2* Sm, int s, double2* X, cudaStream_t st) {
+  if (nleaves <= 0) return;
+  k_leaf_s2m<<<(unsigned)nleaves, LM_T, 0, st>>>(leaf_ids, pofs, slot, lptr, q, Sm, s, X);
+}
+void launch_leaf_l2t(int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, const int32_t* slot,
+                     const int64_t* lptr, const double2* Y, const double2* Tm, int s, double2* outm, cudaStream_t st) {
+  if (nleaves <= 0) return;
+  k_leaf_l2t<<<(unsigned)nleaves, LM_T, (size_t)s * sizeof(double2), st>>>(leaf_ids, pofs, slot, lptr, Y, Tm, s, outm);
+}
+
 // ---------------------------------------------------------------- H8 L2T
 // out_i += sum_b [G(x_i, b) + alpha dG/dn_x(x_i, b)] rho[leaf][b] over the leaf's incoming equivalent
 // surface (E_dn of eq_eval2t).  rho = conj(U) Sigma^-1 y~ (eq_cmpt) comes from the

@@ -49,6 +49,17 @@ void launch_s2m_check(int kind, int64_t nleaves, const int32_t* leaf_ids, LeafGe
 // H8: out += E_dn rho over the leaves' equivalent surfaces; rho[t][b] for leaf leaf_ids[t]
 void launch_l2t_eval(int64_t nleaves, const int32_t* leaf_ids, LeafGeom L, Points P, const double* surf, int nsurf,
                      double k, double2 alpha, const double2* rho, double2* outm, cudaStream_t st);
+// Stored leaf S2M / L2T matrices ("precomputed and saved in memory"): rows per point of the
+// owned leaves of one LF level, pofs[t] = first row of owned leaf t.  launch_leafmat builds Sm = (Sigma^-1 U^H)
+// E_up (Sred: s x nsurf column-major) and Tm = E_dn (conj(U) Sigma^-1) (TredT: nsurf x s row-major); the apply
+// kernels then compute X[slot] = S_leaf q and out += T_leaf Y[slot].
+void launch_leafmat(int kind, int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, LeafGeom L, Points P,
+                    const double* surf, int nsurf, double k, double2 alpha, double2 alpha_dn, const double2* Sred,
+                    const double2* TredT, int s, double2* Sm, double2* Tm, cudaStream_t st);
+void launch_leaf_s2m(int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, const int32_t* slot,
+                     const int64_t* lptr, const double2* q, const double2* Sm, int s, double2* X, cudaStream_t st);
+void launch_leaf_l2t(int64_t nleaves, const int32_t* leaf_ids, const int64_t* pofs, const int32_t* slot,
+                     const int64_t* lptr, const double2* Y, const double2* Tm, int s, double2* outm, cudaStream_t st);
 // Grouped translation (H5 M2M, H6 M2L, H7 L2L): one CTA per work item; an item owns a
 // disjoint set of output slots and walks a list of groups, each group = one matrix
 // (dense s_out x s_in, or low-rank U (s_out x r) V (r x s_in)) applied to its pairs:

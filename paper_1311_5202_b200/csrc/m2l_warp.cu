@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
         m2l_task<(RTMAX >= 2 ? 2 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 3 || RTMAX == 3)
         m2l_task<(RTMAX >= 3 ? 3 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
-      else if (rt == 4 || RTMAX == 4)
+      else if (rt == 4 || RTMAX == 4)  // (the launcher picks RTMAX >= the launch's largest rank / 8)
         m2l_task<(RTMAX >= 4 ? 4 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else
         m2l_task<(RTMAX >= 5 ? 5 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
@@ -225,7 +225,8 @@ cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaS
   // still fit (FDA_M2L_SUM3=0: never; FDA_M2L_OCC=2: at most two CTAs per SM)
   const size_t sm2 = (size_t)T.mmax * sizeof(double), sm3 = sm2 * 3 / 2;
   const size_t third = 74 * 1024;
-  const bool big = sm2 > (size_t)GT_SMEM_BUDGET;
+  // (ranks above 32 need the RTMAX = 5 instantiation, which only the 16-warp configuration has)
+  const bool big = sm2 > (size_t)GT_SMEM_BUDGET || T.rmax8 > 32;
   const bool allow3 = !(getenv("FDA_M2L_SUM3") && getenv("FDA_M2L_SUM3")[0] == '0');
   const bool occ3 =
       !big && T.rmax8 <= 16 && sm2 <= third && !(getenv("FDA_M2L_OCC") && getenv("FDA_M2L_OCC")[0] == '2');

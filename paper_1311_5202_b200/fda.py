@@ -53,7 +53,8 @@ class fda_stats(ctypes.Structure):
                 ("setup_tree_s", "setup_lists_s", "setup_ops_s", "setup_upload_s", "flops_p2p", "flops_m2l",
                  "flops_m2m", "flops_l2l", "flops_s2m", "flops_l2t", "bytes_csr")] + \
                [(f, ctypes.c_int64) for f in ("s2m_evals", "l2t_evals", "xchg_send_bytes", "xchg_recv_bytes",
-                                                 "m2l_ops")]
+                                                 "m2l_ops")] + \
+               [(f, ctypes.c_double) for f in ("bytes_s2m", "bytes_l2t")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -58,3 +58,36 @@ def test_warp_task_m2l_equals_chunk_m2l(name, nu, k):
     print(f"{name}: N={p.N} warp-task vs chunk far field rel l2 {err:.3e}")
     assert np.isfinite(a).all()
     assert err <= 1e-12
+
+
+def test_warp_task_m2l_high_ranks_eps_1e6():
+    """eps = 1e-6: longer expansions and ranks up to 40 (five V row tiles) on every level; the launch must pick
+    the instantiation whose RTMAX covers its largest rank."""
+    p = synth.make_problem("x", k=50.0, nu=16)
+    phi = synth.random_phi(p.N, 5)
+    a = _far_eps(p, phi, True, 1e-6)
+    b = _far_eps(p, phi, False, 1e-6)
+    err = oracle.rel_l2(a, b)
+    print(f"eps=1e-6 N={p.N}: warp-task vs chunk far field rel l2 {err:.3e}")
+    assert err <= 1e-11
+
+
+def _far_eps(p, phi, warp, eps):
+    fda = _fda()
+    old = os.environ.get("FDA_M2L_WARP")
+    os.environ["FDA_M2L_WARP"] = "1" if warp else "0"
+    try:
+        h = fda.fda_plan_create(_dev(p.x), _dev(p.n), _dev(p.w), p.k, p.alpha, eps, fda.fda_options_default())
+    finally:
+        if old is None:
+            del os.environ["FDA_M2L_WARP"]
+        else:
+            os.environ["FDA_M2L_WARP"] = old
+    try:
+        d_phi = _dev(phi.view(np.float64))
+        d_out = torch.empty_like(d_phi)
+        fda.fda_apply_phases(h, fda.FDA_PHASE_FAR, d_phi, d_out)
+        torch.cuda.synchronize()
+    finally:
+        fda.fda_plan_destroy(h)
+    return d_out.cpu().numpy().view(np.complex128)

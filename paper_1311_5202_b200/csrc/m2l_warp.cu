@@ -147,9 +147,11 @@ __device__ __forceinline__ void m2l_task(const double* __restrict__ Ms, int kin,
 
 // NS: doubles per staged operator tile (64, or 96 with the 3M sums); RTMAX: largest V row-tile count of the
 // launch's groups; MINB: CTAs per SM the registers are budgeted for
+// cap: the dynamic shared memory in doubles; in an NS = 64 launch, groups of rank <= 16 whose operator with the
+// 3M sums still fits cap (the low ranks of a launch sized for rank 24) are staged and run with the sums
 template <int NS, int RTMAX, int MINB, int MW_T>
 __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2* __restrict__ X,
-                                                         double2* __restrict__ Y) {
+                                                         double2* __restrict__ Y, int cap) {
   extern __shared__ double msm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s_in = T.s_in, s_out = T.s_out;
@@ -164,10 +166,11 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
     if (rt <= 0) continue;  // rank 0: nothing to add
     // stage the group's operator (V then U, fragment order, contiguous)
     __syncthreads();  // the previous group's operator is no longer read
+    const int ntile = rt * kin + mout * 2 * rt;
+    const bool g96 = NS == 96 || (rt <= 2 && ntile * 96 <= cap);
     {
       const double* src = T.pool + T.gmat[grp];
-      const int ntile = rt * kin + mout * 2 * rt;
-      if (NS == 64) {
+      if (!g96) {
         for (int i = tid; i < ntile * 32; i += MW_T) cp_async16_w(msm + 2 * i, src + 2 * i);
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
       } else {  // tiles of 96: the real and imaginary parts and their sum (the 3M operand), summed once here
@@ -183,7 +186,12 @@ __global__ void __launch_bounds__(MW_T, MINB) k_m2l_warp(GTrans T, const double2
     const int64_t ntask = (pe - pb + 7) / 8;
     for (int64_t task = warp; task < ntask; task += MW_T / 32) {
       const int64_t p0 = pb + 8 * task;
-      if (rt == 1 || RTMAX == 1)
+      if (NS == 64 && g96) {  // low ranks with the sums staged
+        if (rt == 1)
+          m2l_task<1, 96, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+        else
+          m2l_task<2, 96, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
+      } else if (rt == 1 || RTMAX == 1)
         m2l_task<1, NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
       else if (rt == 2 || RTMAX == 2)
         m2l_task<(RTMAX >= 2 ? 2 : 1), NS, (MINB >= 3 ? 2 : 4)>(msm, kin, kt1, mo, kt2, s_in, s_out, so_own, X, Y, T.in, T.out, p0, pe, lane);
@@ -232,7 +240,7 @@ cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaS
       !big && T.rmax8 <= 16 && sm2 <= third && !(getenv("FDA_M2L_OCC") && getenv("FDA_M2L_OCC")[0] == '2');
   const bool sum3 = allow3 && sm3 <= (big ? smem_optin_bytes() : occ3 ? third : (size_t)GT_SMEM_BUDGET);
   const size_t sm = sum3 ? sm3 : sm2;
-  void (*kern)(GTrans, const double2*, double2*) =
+  void (*kern)(GTrans, const double2*, double2*, int) =
       big ? (sum3 ? k_m2l_warp<96, 5, 1, 512> : k_m2l_warp<64, 5, 1, 512>)
           : occ3 ? (sum3 ? k_m2l_warp<96, 2, 3, 256> : k_m2l_warp<64, 2, 3, 256>)
                  : (sum3 ? k_m2l_warp<96, 4, 2, 256> : k_m2l_warp<64, 4, 2, 256>);
@@ -240,7 +248,7 @@ cudaError_t launch_m2l_warp(const GTrans& T, const double2* X, double2* Y, cudaS
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  kern<<<(unsigned)T.n_items, big ? 512 : 256, sm, st>>>(T, X, Y);
+  kern<<<(unsigned)T.n_items, big ? 512 : 256, sm, st>>>(T, X, Y, allow3 ? (int)(sm / sizeof(double)) : 0);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
 """profiles/r02/traffic.json from an ncu launch list of the bench command (tools/jobs/r02_ncu.sh,
-`-k regex:"k_(gtrans|p2p|csr|s2m|l2t|permute|unpermute|xpack|xunpack)"`, metrics gpu__time_duration.sum and
+`-k regex:"k_(gtrans|m2l_warp|p2p|csr|s2m|l2t|leaf_s2m|leaf_l2t|permute|unpermute|xpack|xunpack)"`, metrics gpu__time_duration.sum and
 dram__bytes_{read,write}.sum): DRAM bytes (read + write) per apply, summed over the launches of each
 phase of the second apply in the list.  Launch order of api.cu's apply: permute, p2p, csr, then per LF
 leaf level (S2M check + product), the M2M transitions, the M2L launches (one or two per level), the
@@ -33,9 +33,12 @@ def main():
     starts = [j for j, i in enumerate(order) if "k_permute_scale" in per[i]["name"]]
     a, b = starts[1], (starts[2] if len(starts) > 2 else len(order))
     ids = order[a:b]
-    nm2l = len(ids) - 4 - 4 * nlf - 2 * ntr
-    seq = ["permute", "p2p", "csr"] + ["s2m"] * (2 * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
-          ["l2t"] * (2 * nlf) + ["unpermute"]
+    # stored leaf matrices (k_leaf_s2m / k_leaf_l2t): one launch per LF leaf level each; else two (surface
+    # evaluation + product)
+    per_lf = 1 if any("k_leaf_s2m" in per[i]["name"] for i in ids) else 2
+    nm2l = len(ids) - 4 - 2 * per_lf * nlf - 2 * ntr
+    seq = ["permute", "p2p", "csr"] + ["s2m"] * (per_lf * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
+          ["l2t"] * (per_lf * nlf) + ["unpermute"]
     assert len(seq) == len(ids), (len(seq), len(ids))
     res = {}
     for ph, i in zip(seq, ids):

@@ -11,3 +11,5 @@ timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
 echo "launch exit $?" >> gpurun_out/ncu_launch.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
 timeout 2400 python -m pytest tests -m gpu -q -s -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+# the top kernel (the LF level-8 warp-task M2L launch of the first apply), once per build
+K=k_m2l_warp S=3 OUT=prof_m2l8_final bash tools/jobs/ncu_m2l.sh

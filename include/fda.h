@@ -109,6 +109,9 @@ typedef struct {
   int32_t original;        /* 1: the paper's "original" FDA for Table 1: expansions are the
                               equivalent densities (no SVD reduction of the basis), dense unreduced M2L, no low
                               rank (R24); default 0 = the improved FDA */
+  int32_t graph;           /* 1 (default): fda_apply replays a CUDA graph of its device-resident middle (near field,
+                              upward pass, M2L, L2L, L2T; captured on the second apply of a phase mask, single-rank
+                              plans; fda_plan_set_correction drops it); 0 (or env FDA_GRAPH=0): plain launches */
 } fda_options;
 
 typedef struct {

@@ -103,6 +103,13 @@ struct fda_plan_s {
   cudaEvent_t ev_up = nullptr, ev_x = nullptr;
   cudaStream_t nstream = nullptr;  // near field (P2P, correction), concurrent with the far field
   cudaEvent_t ev_perm = nullptr, ev_near = nullptr;
+  // CUDA graph of the apply's device-resident middle (near field, upward pass, M2L, L2L, L2T): captured once per
+  // phase mask on the plan's capture stream, replayed on the caller's stream between the permute and the
+  // unpermute (which take the caller's pointers).  fda_options.graph / FDA_GRAPH; single-rank plans.
+  bool graph_on = false;
+  cudaStream_t gstream = nullptr;
+  std::map<uint32_t, cudaGraphExec_t> gexec;
+  std::map<uint32_t, int> gcalls;  // applies per mask so far (the capture is the second one: lazy setup done)
   // correction
   int64_t nnz = 0;
   int64_t* c_ptr = nullptr;
@@ -139,6 +146,7 @@ bool is_device_ptr(const void* p) {
 struct CudaFail {
   fda_status s;
 };
+void drop_graphs(fda_plan P);
 
 // FDA_DEBUG=1: report the failing call site on stderr
 void ck_at(cudaError_t e, int line) {
@@ -1403,6 +1411,7 @@ void fda_options_default(fda_options* o) {
   o->rank = 0;
   o->nranks = 1;
   o->verbose = 0;
+  o->graph = 1;
 }
 
 const char* fda_status_str(fda_status s) {
@@ -1540,6 +1549,8 @@ fda_status fda_plan_create_ex(int64_t n, const double* points, const double* nor
     ck(cudaStreamCreateWithFlags(&P->nstream, cudaStreamNonBlocking));
     ck(cudaEventCreateWithFlags(&P->ev_perm, cudaEventDisableTiming));
     ck(cudaEventCreateWithFlags(&P->ev_near, cudaEventDisableTiming));
+    P->graph_on = o.graph != 0 && !(getenv("FDA_GRAPH") && getenv("FDA_GRAPH")[0] == '0');
+    if (P->graph_on) ck(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
     ck(cudaDeviceSynchronize());
     P->st.setup_upload_s = now() - t0;
     P->st.device_bytes = P->bytes;
@@ -1579,6 +1590,7 @@ fda_status fda_plan_set_correction(fda_plan P, int64_t nnz, const int64_t* row_p
   if (P->sticky_error) return FDA_ERR_CUDA;
   if (nnz < 0) return FDA_ERR_INVALID_ARG;
   if (nnz > 0 && (!row_ptr || !col || !val)) return FDA_ERR_INVALID_ARG;
+  drop_graphs(P);  // the captured applies hold the old correction's pointers
   try {
     const int64_t n = P->n;
     int64_t* n_ptr = nullptr;
@@ -1835,6 +1847,79 @@ void nccl_allgather_out(fda_plan P, cudaStream_t st) {
   nck(N.GroupEnd());
 }
 
+// the apply between the permute of phi and the unpermute of out: it touches plan buffers only
+void apply_middle(fda_plan P, uint32_t mask, cudaStream_t st, Marks& mk, Trace& tr) {
+  const bool xchg = P->nranks > 1 && has_far(P, mask);
+  // the near field (P2P, correction: H2, H3) runs on the plan's side stream, concurrent with the far
+  // field; L2T (which adds into the same rows) waits for it.  Timed applies run the phases in sequence.
+  const bool overlap = !mk.on && !tr.on && has_far(P, mask);
+  if (overlap) {
+    ck(cudaEventRecord(P->ev_perm, st));
+    ck(cudaStreamWaitEvent(P->nstream, P->ev_perm, 0));
+    stage_near(P, mask, P->nstream, mk);
+    ck(cudaEventRecord(P->ev_near, P->nstream));
+  }
+  stage_up(P, mask, P->xc.sendbuf, st, mk, tr);
+  if (xchg && !mk.on) {
+    // the exchange runs on the plan's exchange stream
+    ck(cudaEventRecord(P->ev_up, st));
+    ck(cudaStreamWaitEvent(P->xstream, P->ev_up, 0));
+    nccl_exchange(P, P->xstream);
+    ck(cudaEventRecord(P->ev_x, P->xstream));
+    if (!overlap) stage_near(P, mask, st, mk);
+    ck(cudaStreamWaitEvent(st, P->ev_x, 0));
+  } else {
+    mk.begin(9);
+    if (xchg) nccl_exchange(P, st);
+    mk.end(9);
+    if (!overlap) stage_near(P, mask, st, mk);
+  }
+  stage_down(P, mask, P->xc.recvbuf, st, mk, tr, overlap ? P->ev_near : nullptr);
+}
+
+void drop_graphs(fda_plan P) {
+  for (auto& kv : P->gexec) cudaGraphExecDestroy(kv.second);
+  P->gexec.clear();
+  P->gcalls.clear();
+}
+
+// replay (capturing it on first use) the CUDA graph of apply_middle for this mask on st; false: run it plainly.
+// The first apply of a mask runs plainly (one-time launch setup: shared-memory attributes, constants), the
+// second one is captured on the plan's capture stream.  A failed capture turns graphs off for the plan.
+bool apply_graph(fda_plan P, uint32_t mask, cudaStream_t st) {
+  auto it = P->gexec.find(mask);
+  if (it == P->gexec.end()) {
+    if (P->gcalls[mask]++ < 1) return false;
+    Marks mk0;
+    Trace tr0;
+    tr0.on = false;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    ck(cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeRelaxed));
+    bool ok = true;
+    try {
+      apply_middle(P, mask, P->gstream, mk0, tr0);
+    } catch (const CudaFail&) {
+      ok = false;
+    }
+    const cudaError_t e = cudaStreamEndCapture(P->gstream, &g);
+    if (ok && e == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+      it = P->gexec.emplace(mask, ex).first;
+    } else {
+      ok = false;
+    }
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      cudaGetLastError();
+      P->graph_on = false;
+      P->logstr += "CUDA graph capture of the apply failed; applies run without a graph\n";
+      return false;
+    }
+  }
+  ck(cudaGraphLaunch(it->second, st));
+  return true;
+}
+
 fda_status check_apply_args(fda_plan P, const void* phi, const void* out) {
   if (!P || !phi || !out) return FDA_ERR_INVALID_ARG;
   if (P->host_only) return FDA_ERR_STATE;
@@ -1875,32 +1960,9 @@ static fda_status apply_impl(fda_plan P, uint32_t mask, const double* phi, doubl
       for (auto& e : mk.ev) ck(cudaEventCreate(&e));
     Trace tr;
     stage_permute(P, d_phi, st, mk);
-    const bool xchg = P->nranks > 1 && has_far(P, mask);
-    // the near field (P2P, correction: H2, H3) runs on the plan's side stream, concurrent with the far
-    // field; L2T (which adds into the same rows) waits for it.  Timed applies run the phases in sequence.
-    const bool overlap = !mk.on && !tr.on && has_far(P, mask);
-    if (overlap) {
-      ck(cudaEventRecord(P->ev_perm, st));
-      ck(cudaStreamWaitEvent(P->nstream, P->ev_perm, 0));
-      stage_near(P, mask, P->nstream, mk);
-      ck(cudaEventRecord(P->ev_near, P->nstream));
-    }
-    stage_up(P, mask, P->xc.sendbuf, st, mk, tr);
-    if (xchg && !mk.on) {
-      // the exchange runs on the plan's exchange stream
-      ck(cudaEventRecord(P->ev_up, st));
-      ck(cudaStreamWaitEvent(P->xstream, P->ev_up, 0));
-      nccl_exchange(P, P->xstream);
-      ck(cudaEventRecord(P->ev_x, P->xstream));
-      if (!overlap) stage_near(P, mask, st, mk);
-      ck(cudaStreamWaitEvent(st, P->ev_x, 0));
-    } else {
-      mk.begin(9);
-      if (xchg) nccl_exchange(P, st);
-      mk.end(9);
-      if (!overlap) stage_near(P, mask, st, mk);
-    }
-    stage_down(P, mask, P->xc.recvbuf, st, mk, tr, overlap ? P->ev_near : nullptr);
+    // CUDA graph of the middle on single-rank plans (untimed, untraced applies)
+    const bool graph = P->graph_on && !mk.on && !tr.on && P->nranks == 1 && !P->comm;
+    if (!(graph && apply_graph(P, mask, st))) apply_middle(P, mask, st, mk, tr);
     mk.begin(8);
     if (P->comm) nccl_allgather_out(P, st);
     fda::launch_unpermute(n, P->perm, P->outm, d_out, st);
@@ -2111,6 +2173,8 @@ fda_status fda_plan_destroy(fda_plan P) {
   if (P->ev_up) cudaEventDestroy(P->ev_up);
   if (P->ev_x) cudaEventDestroy(P->ev_x);
   if (P->xstream) cudaStreamDestroy(P->xstream);
+  drop_graphs(P);
+  if (P->gstream) cudaStreamDestroy(P->gstream);
   if (P->ev_perm) cudaEventDestroy(P->ev_perm);
   if (P->ev_near) cudaEventDestroy(P->ev_near);
   if (P->nstream) cudaStreamDestroy(P->nstream);

@@ -1145,9 +1145,6 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
     };
     // M2M (and its transpose, L2L) operators on the device: one per (parent direction, child octant)
     const double *dup = nullptr, *ddn = nullptr;
-    std::vector<int32_t> tr_rank;          // low-rank transition: rank per operator (empty: dense)
-    std::vector<int64_t> tr_off, tr_offT;  // ... and the factor offsets in the M2M / L2L pools
-    double fup_lr = -1, fdn_lr = -1;
     if (dev_ops && nmat > 0) {
       std::vector<int32_t> ia(nmat), ib(nmat);
       std::vector<double> sh(3 * (size_t)nmat);
@@ -1167,86 +1164,32 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
       set_max(bset[T.lp + 1], &J.maxn);
       J.maxs = std::max(T.sp, T.sc);
       const int64_t szu = frag_size(-1, T.sp, T.sc), szd = frag_size(-1, T.sc, T.sp);
-      std::vector<int64_t> off(nmat), offT(nmat);
-      for (int64_t t = 0; t < nmat; ++t) off[t] = t * szu, offT[t] = t * szd;
-      // Low-rank LF -> HF transitions (FDA_M2M_LR = f > 0, R27): the M2M operator from a child's LF
-      // expansion (s ~ 136) into a parent wedge (s ~ 60-72) is compressed like the M2L's K~ (PAPER.md:834-856,
-      // sigma_i < f eps_lr sigma_1, low rank iff 2 r < s), L2L takes the transposed factors.  Used only when every
-      // operator of the transition is low rank (one launch kind per transition).
-      const double m2m_lr = getenv("FDA_M2M_LR") ? atof(getenv("FDA_M2M_LR")) : 0.0;
-      if (m2m_lr > 0 && H.opt.lowrank && Lp.hf && !Lc.hf) {
-        int32_t* d_rank = dalloc<int32_t>(P, nmat);
-        J.compress = 1, J.eps_lr = m2m_lr * H.eps_lr_level(Lp), J.rank = d_rank;
-        if (getenv("FDA_RANK_ROUND")) J.rank_round = std::max(1, atoi(getenv("FDA_RANK_ROUND")));
-        ck(fda::launch_opjob(J, 1, 0));
-        std::vector<int32_t> rk(nmat);
-        ck(cudaMemcpy(rk.data(), d_rank, nmat * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        bool all = true;
-        for (int32_t r : rk) all &= r >= 0 && pad8(r) <= 40;
-        if (all) {
-          int64_t tu = 0, td = 0;
-          for (int64_t t = 0; t < nmat; ++t) {
-            off[t] = tu, offT[t] = td;
-            tu += frag_size(rk[t], T.sp, T.sc), td += frag_size(rk[t], T.sc, T.sp);
-          }
-          tr_rank = rk;
-          J.rank_in = d_rank;
-          J.offT = upload(P, offT);
-        } else {
-          J.compress = 0;
-        }
-      }
-      const int64_t nu = tr_rank.empty() ? nmat * szu : off.back() + frag_size(tr_rank.back(), T.sp, T.sc);
-      const int64_t nd = tr_rank.empty() ? nmat * szd : offT.back() + frag_size(tr_rank.back(), T.sc, T.sp);
-      double* pu = dalloc<double>(P, (size_t)nu);
-      double* pd = dalloc<double>(P, (size_t)nd);
+      std::vector<int64_t> off(nmat);
+      for (int64_t t = 0; t < nmat; ++t) off[t] = t * szu;
+      double* pu = dalloc<double>(P, (size_t)(nmat * szu));
+      double* pd = dalloc<double>(P, (size_t)(nmat * szd));
       J.off = upload(P, off), J.pool = pu, J.poolT = pd;
       ck(fda::launch_opjob(J, 2, 0));
       dup = pu, ddn = pd;
-      tr_off = off, tr_offT = offT;
     }
-    // low-rank transition: the groups' ranks and factor offsets; flops 8 r (s_out + s_in) per pair
-    auto lowrank_groups = [&](GroupedPairs& G, const std::vector<int64_t>& offs, bool up) {
-      double f = 0;
-      for (int64_t g = 0; g < nmat; ++g) {
-        const double np = (double)(G.gptr[g + 1] - G.gptr[g]);
-        G.rank[g] = tr_rank[g], G.mat[g] = offs[g];
-        f += np * 8.0 * tr_rank[g] * ((double)G.so[g] + (double)G.si[g]);
-      }
-      (up ? fup_lr : fdn_lr) = f;
-    };
     if (!T.up_child.empty()) {
       GroupedPairs G = grouped(T.up_ptr, T.up_child, T.up_mat, up_keep);
       sizes(G, true);
-      if (!tr_rank.empty())
-        lowrank_groups(G, tr_off, true);
-      else if (dev_ops)
+      if (dev_ops)
         for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sp, T.sc);
       D.up = make_items(P, G, Lp.out_cube, Lp.out_dir, (int64_t)Lp.cubes.size(), T.sp, T.sc,
                         dev_ops ? nullptr : T.pool.data(), dup);
-      D.up.warp_tasks = !tr_rank.empty() && fda::m2l_warp_on();
     }
     if (!T.dn_parent.empty()) {
       GroupedPairs G = grouped(T.dn_ptr, T.dn_parent, T.dn_mat, dn_keep);
       sizes(G, false);
-      if (!tr_rank.empty())
-        lowrank_groups(G, tr_offT, false);
-      else if (dev_ops)
+      if (dev_ops)
         for (auto& m : G.mat) m = (m / ((int64_t)T.sp * T.sc)) * frag_size(-1, T.sc, T.sp);
       D.dn = make_items(P, G, Lc.in_cube, Lc.in_dir, (int64_t)Lc.cubes.size(), T.sc, T.sp,
                         dev_ops ? nullptr : T.poolT.data(), ddn);
-      D.dn.warp_tasks = !tr_rank.empty() && fda::m2l_warp_on();
     }
-    P->st.flops_m2m += fup_lr >= 0 ? fup_lr : 0.5 * fup;  // keep() runs twice per pair (count, fill)
-    P->st.flops_l2l += fdn_lr >= 0 ? fdn_lr : 0.5 * fdn;
-    if (H.opt.verbose && !tr_rank.empty()) {
-      std::map<int, int64_t> hist;
-      for (int32_t r : tr_rank) hist[r]++;
-      std::ostringstream os;
-      os << "m2m/l2l L" << T.lp << "<-L" << T.lp + 1 << " low rank (s " << T.sp << " x " << T.sc << "): operators by rank:";
-      for (const auto& kv : hist) os << " " << kv.first << ":" << kv.second;
-      H.log += os.str() + "\n";
-    }
+    P->st.flops_m2m += 0.5 * fup;  // keep() runs twice per pair (count, fill)
+    P->st.flops_l2l += 0.5 * fdn;
     P->tr.push_back(D);
   }
   lap("m2m/l2l");

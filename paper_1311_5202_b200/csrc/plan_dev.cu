@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
     if (rank < 0) {
       frag_write(dst, sA, sB, pd_pad8(J.s_out), pd_pad4(J.s_in), [&](int i, int j) { return O[i + (size_t)j * sA]; });
       if (J.poolT) {
-        double* dT = J.poolT + (J.offT ? J.offT[it] : (int64_t)it * ((int64_t)pd_pad8(J.s_in) / 8) * (pd_pad4(J.s_out) / 4) * 64);
+        double* dT = J.poolT + (int64_t)it * ((int64_t)pd_pad8(J.s_in) / 8) * (pd_pad4(J.s_out) / 4) * 64;
         frag_write(dT, sB, sA, pd_pad8(J.s_in), pd_pad4(J.s_out), [&](int i, int j) { return O[j + (size_t)i * sA]; });
       }
     } else {
@@ -306,16 +306,6 @@ __global__ void __launch_bounds__(OP_T) k_opjob(OpJob J, int pass, double2* ws, 
       });
       double* du = dst + (int64_t)(pd_pad8(rank) / 8) * (pd_pad4(J.s_in) / 4) * 64;
       frag_write(du, sA, rank, pd_pad8(J.s_out), pd_pad8(rank), [&](int i, int j) { return U[i + (size_t)j * sA]; });
-      if (J.poolT) {
-        // low-rank M2M: L2L = M~^T = (U^ V^)^T = V^^T U^^T, i.e. first factor U^^T (r x sA), then V^^T (sB x r)
-        double* dT = J.poolT + J.offT[it];
-        frag_write(dT, rank, sA, pd_pad8(rank), pd_pad4(J.s_out), [&](int i, int j) { return U[j + (size_t)i * sA]; });
-        double* duT = dT + (int64_t)(pd_pad8(rank) / 8) * (pd_pad4(J.s_out) / 4) * 64;
-        frag_write(duT, sB, rank, pd_pad8(J.s_in), pd_pad8(rank), [&](int i, int j) {
-          const double2 w = W[i + (size_t)sel[j] * sB];
-          return make_double2(w.x, -w.y);
-        });
-      }
     }
     __syncthreads();
   }

@@ -44,7 +44,6 @@ struct OpJob {
   const int64_t* off = nullptr;  // pass 2: item -> offset (doubles) into pool
   double* pool = nullptr;        // pass 2 output
   double* poolT = nullptr;       // M2M only: the transposed operator (L2L) at the same offsets
-  const int64_t* offT = nullptr; // M2M with compress: item -> offset (doubles) into poolT (null: the dense stride)
   // workspace
   int maxn = 0, maxs = 0;        // largest set size / expansion length of the job
 };

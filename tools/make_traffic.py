@@ -36,12 +36,19 @@ def main():
     # stored leaf matrices (k_leaf_s2m / k_leaf_l2t): one launch per LF leaf level each; else two (surface
     # evaluation + product)
     per_lf = 1 if any("k_leaf_s2m" in per[i]["name"] for i in ids) else 2
-    nm2l = len(ids) - 4 - 2 * per_lf * nlf - 2 * ntr
-    seq = ["permute", "p2p", "csr"] + ["s2m"] * (per_lf * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
+    # the near field (P2P, correction) runs on a side stream / graph branch: its launches may sit anywhere
+    # between the permute and the unpermute, so they are told apart by name; the far field keeps its order
+    def near_phase(i):
+        nm = per[i]["name"]
+        return "p2p" if "k_p2p" in nm else "csr" if "k_csr" in nm else None
+    near = [(near_phase(i), i) for i in ids if near_phase(i)]
+    far = [i for i in ids if not near_phase(i)]
+    nm2l = len(far) - 2 - 2 * per_lf * nlf - 2 * ntr
+    seq = ["permute"] + ["s2m"] * (per_lf * nlf) + ["m2m"] * ntr + ["m2l"] * nm2l + ["l2l"] * ntr + \
           ["l2t"] * (per_lf * nlf) + ["unpermute"]
-    assert len(seq) == len(ids), (len(seq), len(ids))
+    assert len(seq) == len(far), (len(seq), len(far))
     res = {}
-    for ph, i in zip(seq, ids):
+    for ph, i in list(zip(seq, far)) + near:
         d = per[i]
         res.setdefault(ph, {"dram_bytes": 0.0, "ms": 0.0, "launches": 0})
         res[ph]["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)

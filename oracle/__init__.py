@@ -48,6 +48,8 @@ def _lib():
         lib.oracle_rows.argtypes = [ctypes.c_int, L, V, V, V, D, D, D, V, L, V, V, V, V, V]
         lib.oracle_near.argtypes = [ctypes.c_int, L, V, V, V, D, D, D, V, L, V, V, V, V, V]
         lib.oracle_targets.argtypes = [ctypes.c_int, L, V, V, L, V, V, V, D, D, D, V, V]
+        lib.oracle_moments.argtypes = [ctypes.c_int, V, V, V, L, V, V, D, D, D, ctypes.c_int, V, V, D, ctypes.c_int, V]
+        lib.oracle_weights_from_moments.argtypes = [V, L, V, V]
         lib.oracle_num_threads.restype = ctypes.c_int
         _LIB = lib
     return _LIB
@@ -120,6 +122,31 @@ def apply_targets(kind, tx, tn, y, ny, w, k, alpha, dens) -> np.ndarray:
     out = np.zeros(tx.shape[0], dtype=np.complex128)
     _lib().oracle_targets(kind, tx.shape[0], _p(tx), _p(tn), y.shape[0], _p(y), _p(ny), _p(w), float(k),
                           float(np.real(alpha)), float(np.imag(alpha)), _p(dens), _p(out))
+    return out
+
+
+def element_moments(kind, elem, tx, tn, pair_t, pair_e, k, alpha, nq=12, theta=0.25, maxdepth=24) -> np.ndarray:
+    """I_n = int_Delta K(x_t, y) xi1^p xi2^q dy, (p,q) = (0,0),(1,0),(0,1),(2,0),(1,1),(0,2), per pair
+    (recursive subdivision quadrature).  Returns (npairs, 6) complex."""
+    elem, tx, tn = _f64(elem), _f64(tx), _f64(tn)
+    pt = np.ascontiguousarray(pair_t, dtype=np.int64)
+    pe = np.ascontiguousarray(pair_e, dtype=np.int64)
+    g, w = np.polynomial.legendre.leggauss(int(nq))  # on [-1, 1]
+    gu, gw = _f64(0.5 * (g + 1.0)), _f64(0.5 * w)
+    out = np.zeros((pt.shape[0], 6), dtype=np.complex128)
+    _lib().oracle_moments(kind, _p(elem), _p(tx), _p(tn), pt.shape[0], _p(pt), _p(pe), float(k),
+                          float(np.real(alpha)), float(np.imag(alpha)), int(nq), _p(gu), _p(gw), float(theta),
+                          int(maxdepth), _p(out))
+    return out
+
+
+def corrected_weights(kind, elem, xi, tx, tn, pair_t, pair_e, k, alpha, **kw) -> np.ndarray:
+    """Locally corrected weights wbar_j^Delta(K; x_t): (npairs, 6) complex, j in the order
+    of the quadrature points xi (6 x 2 intrinsic coordinates)."""
+    mom = element_moments(kind, elem, tx, tn, pair_t, pair_e, k, alpha, **kw)
+    xi = _f64(xi)
+    out = np.zeros_like(mom)
+    _lib().oracle_weights_from_moments(_p(xi), mom.shape[0], _p(mom), _p(out))
     return out
 
 

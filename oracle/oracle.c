@@ -165,6 +165,135 @@ void oracle_targets(int kind, int64_t m, const double *tx, const double *tn, int
     }
 }
 
+/*
+ * Locally corrected Nystrom weights of one (field point, element) pair -- SURVEY.md §8(f) row 4,
+ * PAPER.md:299-323.  The element is a 6-node quadratic triangle (corners 1, 2, 3, mid-edges 12, 23, 31,
+ * SPEC.md:82) with intrinsic coordinates (xi1, xi2) on the reference triangle xi1, xi2 >= 0, xi1 + xi2 <= 1:
+ *   y(xi) = sum_a N_a(xi) P_a,  t_1 = dy/dxi1,  t_2 = dy/dxi2,  J = |t_1 x t_2|,  n_y = t_1 x t_2 / J.
+ * Moments (right-hand side of PAPER.md:313-317, eq:local correction):
+ *   I_n = int_Delta K(x, y) phi^(n)(y) dy = int_ref K(x, n_x; y(xi), n_y(xi)) xi1^p xi2^q J(xi) dxi,
+ *   phi^(n) = xi1^p xi2^q, p + q <= 2, ordered (p,q) = (0,0),(1,0),(0,1),(2,0),(1,1),(0,2).
+ * They are "nearly singular when x is close to the element, and ... computed by using a recursive
+ * subdivision quadrature": a sub-triangle A, B, C of the reference triangle is split into its
+ * four mid-point children while its largest mapped edge exceeds theta times the distance from x to the
+ * nearest of y(A), y(B), y(C), y(centroid) (the paper gives no criterion -- DESIGN.md reading R27); otherwise
+ * it is integrated by the nq x nq Gauss-Legendre product rule on the collapsed square,
+ *   xi(u, v) = A + u [(B - A) + v (C - B)],  dxi = 2 |T| u du dv,  (u, v) in [0,1]^2.
+ * The Gauss-Legendre nodes and weights on [0,1] are inputs (gu, gw; numpy.polynomial.legendre.leggauss in the
+ * wrapper).  The field point must not lie on the element (the singular self-element integrals need the method
+ * of [rjj_int], which the paper does not give: out of scope).
+ * The weights solve the 6 x 6 system  sum_j wbar_j phi^(n)(xi_j) = I_n  (eq:local correction) at the element's
+ * six quadrature points xi_j (inputs), by Gaussian elimination with partial pivoting.
+ */
+static void elem_map(const double *P, double a, double b, double *y, double *nv, double *J) {
+    double l1 = 1.0 - a - b, l2 = a, l3 = b;
+    double N[6] = {l1 * (2 * l1 - 1), l2 * (2 * l2 - 1), l3 * (2 * l3 - 1), 4 * l1 * l2, 4 * l2 * l3, 4 * l3 * l1};
+    double d1[6] = {-(4 * l1 - 1), 4 * l2 - 1, 0, 4 * (l1 - l2), 4 * l3, -4 * l3};
+    double d2[6] = {-(4 * l1 - 1), 0, 4 * l3 - 1, -4 * l2, 4 * l2, 4 * (l1 - l3)};
+    double t1[3] = {0, 0, 0}, t2[3] = {0, 0, 0};
+    for (int c = 0; c < 3; ++c) {
+        y[c] = 0;
+        for (int q = 0; q < 6; ++q) {
+            y[c] += N[q] * P[3 * q + c];
+            t1[c] += d1[q] * P[3 * q + c];
+            t2[c] += d2[q] * P[3 * q + c];
+        }
+    }
+    if (nv) {
+        double cr[3] = {t1[1] * t2[2] - t1[2] * t2[1], t1[2] * t2[0] - t1[0] * t2[2], t1[0] * t2[1] - t1[1] * t2[0]};
+        *J = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+        for (int c = 0; c < 3; ++c) nv[c] = cr[c] / *J;
+    }
+}
+
+static double dist3(const double *a, const double *b) {
+    return sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]) + (a[2] - b[2]) * (a[2] - b[2]));
+}
+
+static void moments_rec(int kind, const double *P, const double *x, const double *nx, double k, cplx alpha,
+                        int nq, const double *gu, const double *gw, double theta, int depth, int maxdepth,
+                        const double *A, const double *B, const double *C, cplx *I6) {
+    double yA[3], yB[3], yC[3], yG[3];
+    elem_map(P, A[0], A[1], yA, NULL, NULL);
+    elem_map(P, B[0], B[1], yB, NULL, NULL);
+    elem_map(P, C[0], C[1], yC, NULL, NULL);
+    elem_map(P, (A[0] + B[0] + C[0]) / 3.0, (A[1] + B[1] + C[1]) / 3.0, yG, NULL, NULL);
+    double h = fmax(dist3(yA, yB), fmax(dist3(yB, yC), dist3(yC, yA)));
+    double d = fmin(fmin(dist3(x, yA), dist3(x, yB)), fmin(dist3(x, yC), dist3(x, yG)));
+    if (h > theta * d && depth < maxdepth) {
+        double AB[2] = {0.5 * (A[0] + B[0]), 0.5 * (A[1] + B[1])};
+        double BC[2] = {0.5 * (B[0] + C[0]), 0.5 * (B[1] + C[1])};
+        double CA[2] = {0.5 * (C[0] + A[0]), 0.5 * (C[1] + A[1])};
+        moments_rec(kind, P, x, nx, k, alpha, nq, gu, gw, theta, depth + 1, maxdepth, A, AB, CA, I6);
+        moments_rec(kind, P, x, nx, k, alpha, nq, gu, gw, theta, depth + 1, maxdepth, AB, B, BC, I6);
+        moments_rec(kind, P, x, nx, k, alpha, nq, gu, gw, theta, depth + 1, maxdepth, CA, BC, C, I6);
+        moments_rec(kind, P, x, nx, k, alpha, nq, gu, gw, theta, depth + 1, maxdepth, AB, BC, CA, I6);
+        return;
+    }
+    double area2 = fabs((B[0] - A[0]) * (C[1] - A[1]) - (B[1] - A[1]) * (C[0] - A[0])); /* 2 |T| */
+    for (int a = 0; a < nq; ++a)
+        for (int b = 0; b < nq; ++b) {
+            double u = gu[a], v = gu[b];
+            double s1 = A[0] + u * ((B[0] - A[0]) + v * (C[0] - B[0]));
+            double s2 = A[1] + u * ((B[1] - A[1]) + v * (C[1] - B[1]));
+            double y[3], ny[3], J;
+            elem_map(P, s1, s2, y, ny, &J);
+            cplx f = kernel(kind, x, nx, y, ny, k, alpha) * (gw[a] * gw[b] * u * area2 * J);
+            I6[0] += f;
+            I6[1] += f * s1;
+            I6[2] += f * s2;
+            I6[3] += f * s1 * s1;
+            I6[4] += f * s1 * s2;
+            I6[5] += f * s2 * s2;
+        }
+}
+
+/* moments I_n of npairs (field point, element) pairs: elem (ne x 6 x 3), tx / tn (nt x 3), pair_t / pair_e */
+void oracle_moments(int kind, const double *elem, const double *tx, const double *tn, int64_t npairs,
+                    const int64_t *pair_t, const int64_t *pair_e, double k, double ar, double ai, int nq,
+                    const double *gu, const double *gw, double theta, int maxdepth, double *out) {
+    cplx alpha = ar + I * ai;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t p = 0; p < npairs; ++p) {
+        cplx I6[6] = {0, 0, 0, 0, 0, 0};
+        const double A[2] = {0, 0}, B[2] = {1, 0}, C[2] = {0, 1};
+        moments_rec(kind, elem + 18 * pair_e[p], tx + 3 * pair_t[p], tn + 3 * pair_t[p], k, alpha, nq, gu, gw, theta,
+                    0, maxdepth, A, B, C, I6);
+        for (int n = 0; n < 6; ++n) out[12 * p + 2 * n] = creal(I6[n]), out[12 * p + 2 * n + 1] = cimag(I6[n]);
+    }
+}
+
+/* wbar (npairs x 6 complex) from the moments: sum_j wbar_j xi1_j^p xi2_j^q = I_n; xi (6 x 2) quadrature points */
+void oracle_weights_from_moments(const double *xi, int64_t npairs, const double *mom, double *wbar) {
+    for (int64_t p = 0; p < npairs; ++p) {
+        double M[6][6];
+        cplx rhs[6];
+        for (int j = 0; j < 6; ++j) {
+            double a = xi[2 * j], b = xi[2 * j + 1];
+            M[0][j] = 1, M[1][j] = a, M[2][j] = b, M[3][j] = a * a, M[4][j] = a * b, M[5][j] = b * b;
+        }
+        for (int n = 0; n < 6; ++n) rhs[n] = mom[12 * p + 2 * n] + I * mom[12 * p + 2 * n + 1];
+        for (int c = 0; c < 6; ++c) {
+            int piv = c;
+            for (int r = c + 1; r < 6; ++r)
+                if (fabs(M[r][c]) > fabs(M[piv][c])) piv = r;
+            for (int q = 0; q < 6; ++q) { double t = M[c][q]; M[c][q] = M[piv][q]; M[piv][q] = t; }
+            cplx t = rhs[c]; rhs[c] = rhs[piv]; rhs[piv] = t;
+            for (int r = c + 1; r < 6; ++r) {
+                double f = M[r][c] / M[c][c];
+                for (int q = c; q < 6; ++q) M[r][q] -= f * M[c][q];
+                rhs[r] -= f * rhs[c];
+            }
+        }
+        for (int r = 5; r >= 0; --r) {
+            cplx s = rhs[r];
+            for (int q = r + 1; q < 6; ++q) s -= M[r][q] * (wbar[12 * p + 2 * q] + I * wbar[12 * p + 2 * q + 1]);
+            s /= M[r][r];
+            wbar[12 * p + 2 * r] = creal(s), wbar[12 * p + 2 * r + 1] = cimag(s);
+        }
+    }
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);

@@ -211,6 +211,34 @@ fda_status fda_apply_down(fda_plan plan, const double* recvbuf, double* out);
 fda_status fda_plan_export_exchange(fda_plan plan, int peer, int recv, int64_t* count, int32_t* level, int64_t* slot,
                                     int64_t* cube_ijk);
 
+/* Locally corrected Nystrom weights on the device.
+ * For every listed pair (field point t, element e) with the field point OFF the element, the six weights
+ *   wbar_j^Delta(K; x_t),  sum_j wbar_j phi^(n)(xi_j) = int_Delta K(x_t, y) phi^(n)(y) dy,
+ *   phi^(n) = xi1^p xi2^q, p + q <= 2, (p,q) = (0,0),(1,0),(0,1),(2,0),(1,1),(0,2)
+ * with the nearly singular moments computed by recursive subdivision quadrature: a sub-triangle of
+ * the reference triangle is split at its edge mid-points while its largest mapped edge exceeds theta x the
+ * distance from x_t to the nearest of its mapped corners and centroid; leaves take the nq x nq Gauss-Legendre
+ * product rule on the collapsed square (R27).  The self element (x_t on Delta) is singular / hyper-
+ * singular and needs the method of [rjj_int], which the paper does not give: such a pair
+ * makes the call return FDA_ERR_INVALID_ARG (outputs then unspecified).
+ *   kernel        FDA_KERNEL_BMH / _BMG / _T1; k >= 0; alpha = alpha_re + i alpha_im
+ *   elem_nodes    ne x 6 x 3 doubles: corners 1 2 3 then mid-edge nodes 12 23 31 of each quadratic triangle
+ *                 (counter-clockwise seen from outside: n_y = t_1 x t_2 / |t_1 x t_2|)
+ *   xi, wref      the element rule: 6 x 2 intrinsic coordinates (xi1, xi2) on the reference triangle
+ *                 xi1, xi2 >= 0, xi1 + xi2 <= 1, and 6 reference weights (sum 1/2; w_j = wref_j J(xi_j))
+ *   tx, tn        nt x 3 field points and their unit normals
+ *   pair_t/pair_e npairs indices into tx / elem_nodes (int64)
+ *   nq, theta, max_depth   0 selects the defaults 8, 0.5, 16; limits nq <= 16, theta in (0, 1], max_depth <= 20
+ *   wbar          npairs x 6 complex128 (12 doubles per pair), the weights; may be NULL
+ *   delta         npairs x 6 complex128, wbar_j - w_j K(x_t, y_j): the value the correction CSR of
+ *                 fda_plan_set_correction holds for (row t, column of node j of e); may be NULL (not both)
+ * Arrays may be host or device memory; the call synchronises.  Errors: FDA_ERR_INVALID_ARG (arguments, an index
+ * out of range, a field point on its element), FDA_ERR_CUDA (no device / CUDA error), FDA_ERR_OOM. */
+fda_status fda_nystrom_weights(int kernel, double k, double alpha_re, double alpha_im, const double* elem_nodes,
+                               int64_t ne, const double* xi, const double* wref, const double* tx, const double* tn,
+                               int64_t nt, const int64_t* pair_t, const int64_t* pair_e, int64_t npairs, int nq,
+                               double theta, int max_depth, double* wbar, double* delta);
+
 fda_status fda_plan_destroy(fda_plan plan);
 const char* fda_status_str(fda_status s);
 

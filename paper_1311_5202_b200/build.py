@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfda.so")
 SOURCES = ["api.cu", "kernels.cu", "plan.cpp", "linalg.cpp", "nccl_dl.cpp", "plan_dev.cu", "tree_dev.cu", "lists_dev.cu",
-           "m2l_block.cu", "m2l_warp.cu"]
+           "m2l_block.cu", "m2l_warp.cu", "nystrom.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HOSTFLAGS = "-O3,-fPIC,-fopenmp,-march=x86-64-v3,-fcx-limited-range"
 

@@ -32,7 +32,7 @@ EXPORTS = ("fda_options_default", "fda_plan_create", "fda_plan_create_ex", "fda_
            "fda_apply_phases", "fda_apply_timed", "fda_plan_set_stream", "fda_plan_stats", "fda_plan_log",
            "fda_plan_export_leaves", "fda_plan_export_p2p", "fda_plan_export_m2l", "fda_plan_destroy",
            "fda_status_str", "fda_plan_launches", "fda_nccl_unique_id", "fda_plan_create_dist", "fda_dist_counts",
-           "fda_apply_up", "fda_apply_down", "fda_plan_export_exchange")
+           "fda_apply_up", "fda_apply_down", "fda_plan_export_exchange", "fda_nystrom_weights")
 
 
 class fda_options(ctypes.Structure):
@@ -90,6 +90,8 @@ _lib.fda_dist_counts.argtypes = [_P, _P, _P]
 _lib.fda_apply_up.argtypes = [_P, _P, _P]
 _lib.fda_apply_down.argtypes = [_P, _P, _P]
 _lib.fda_plan_export_exchange.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), _P, _P, _P]
+_lib.fda_nystrom_weights.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _I64, _P, _P,
+                                     _P, _P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_double, ctypes.c_int, _P, _P]
 
 
 class FDAError(RuntimeError):
@@ -253,6 +255,20 @@ def fda_plan_export_exchange(plan, peer: int, recv: bool):
     _check(_lib.fda_plan_export_exchange(plan, int(peer), int(recv), ctypes.byref(cnt), _ptr(lev), _ptr(slot),
                                          _ptr(ijk)), "fda_plan_export_exchange")
     return lev, slot, ijk
+
+
+def fda_nystrom_weights(kernel, k, alpha, elem_nodes, xi, wref, tx, tn, pair_t, pair_e, wbar=None, delta=None,
+                        nq=0, theta=0.0, max_depth=0):
+    """Locally corrected weights of (field point, element) pairs (include/fda.h).  elem_nodes (ne, 6, 3),
+    xi (6, 2), wref (6), tx / tn (nt, 3), pair_t / pair_e int64 (npairs); wbar / delta (npairs, 6) complex128,
+    filled in place (numpy arrays or torch tensors, host or device)."""
+    alpha = complex(alpha)
+    ne = int(elem_nodes.shape[0])
+    nt = int(tx.shape[0])
+    npairs = int(pair_t.shape[0])
+    _check(_lib.fda_nystrom_weights(int(kernel), float(k), alpha.real, alpha.imag, _ptr(elem_nodes), ne, _ptr(xi),
+                                    _ptr(wref), _ptr(tx), _ptr(tn), nt, _ptr(pair_t), _ptr(pair_e), npairs, int(nq),
+                                    float(theta), int(max_depth), _ptr(wbar), _ptr(delta)), "fda_nystrom_weights")
 
 
 def fda_plan_destroy(plan):

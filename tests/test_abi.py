@@ -40,6 +40,15 @@ def test_status_strings_and_no_gpu_behaviour():
     # without a device the product path fails loudly (no CPU fallback)
     with pytest.raises(fda.FDAError, match="FDA_ERR_CUDA"):
         fda.fda_plan_create(x, n, w, 1.0, 1j, 1e-4)
+    # the same for the corrected Nystrom weights: argument checks first, then no device -> FDA_ERR_CUDA
+    el = np.zeros((1, 6, 3))
+    xi = np.array([[0.1, 0.1], [0.8, 0.1], [0.1, 0.8], [0.4, 0.4], [0.2, 0.4], [0.4, 0.2]])
+    pr = np.zeros(1, np.int64)
+    out = np.zeros((1, 6), np.complex128)
+    with pytest.raises(fda.FDAError, match="INVALID_ARG"):
+        fda.fda_nystrom_weights(fda.FDA_KERNEL_BMH, 1.0, 1j, el, xi, np.full(6, 1 / 12), x, n, pr, pr, out, nq=40)
+    with pytest.raises(fda.FDAError, match="FDA_ERR_CUDA"):
+        fda.fda_nystrom_weights(fda.FDA_KERNEL_BMH, 1.0, 1j, el, xi, np.full(6, 1 / 12), x, n, pr, pr, out)
 
 
 def test_options_layout():

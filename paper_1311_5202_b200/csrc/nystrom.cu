@@ -13,6 +13,7 @@
 // (every lane takes the same decisions), the nq^2 points of a leaf are spread over the lanes, the six complex
 // moments are reduced by shuffles, lanes 0-5 apply the inverse moment matrix and write wbar_j (and the delta
 // CSR value wbar_j - w_j K(x, y_j) of reading R4).  Fixed evaluation order: results are deterministic.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -62,9 +63,9 @@ __device__ __forceinline__ void ny_map(const double (&P)[18], double a, double b
     }
     const double cx = t1[1] * t2[2] - t1[2] * t2[1], cy = t1[2] * t2[0] - t1[0] * t2[2],
                  cz = t1[0] * t2[1] - t1[1] * t2[0];
-    const double j = sqrt(cx * cx + cy * cy + cz * cz);
-    *J = j;
-    nv[0] = cx / j, nv[1] = cy / j, nv[2] = cz / j;
+    const double j2 = cx * cx + cy * cy + cz * cz, ij = rsqrt(j2);
+    *J = j2 * ij;
+    nv[0] = cx * ij, nv[1] = cy * ij, nv[2] = cz * ij;
   }
 }
 
@@ -92,20 +93,27 @@ struct NyTri {
 
 // flag bits: 1 = pair index out of range, 2 = field point on the element (subdivision unresolved at max_depth)
 template <int KERNEL>
-__global__ void __launch_bounds__(32 * NY_WARPS)
+__global__ void __launch_bounds__(32 * NY_WARPS, 4)
     k_nystrom_weights(const double* __restrict__ elem, int64_t ne, const double* __restrict__ tx,
                       const double* __restrict__ tn, int64_t nt, const int64_t* __restrict__ pair_t,
                       const int64_t* __restrict__ pair_e, int64_t npairs, double k, double2 alpha, int nq,
                       double theta, int max_depth, double2* __restrict__ wbar, double2* __restrict__ delta,
-                      int* __restrict__ flag) {
+                      int* __restrict__ flag, unsigned long long* __restrict__ next) {
   __shared__ NyTri stack[NY_WARPS][NY_STACK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = (int64_t)blockIdx.x * NY_WARPS + warp;
+  // Persistent warps take pairs from a device counter: the work per pair varies by two orders of magnitude
+  // with the distance of the field point (a far element of D_i is one leaf, an adjacent one ~50), so a fixed
+  // pair -> warp map leaves most resident warps idle (ncu: 6.6 of 64 warps active per SM, 26 Mpairs/s).
+  // The result of a pair does not depend on which warp computes it.
+  for (;;) {
+  long long p = 0;
+  if (lane == 0) p = (long long)atomicAdd(next, 1ull);
+  p = __shfl_sync(0xffffffffu, p, 0);
   if (p >= npairs) return;
   const int64_t t = pair_t[p], e = pair_e[p];
   if (t < 0 || t >= nt || e < 0 || e >= ne) {
     if (lane == 0) atomicOr(flag, 1);
-    return;
+    continue;
   }
   double P[18], x[3], nx[3];
 #pragma unroll
@@ -126,13 +134,24 @@ __global__ void __launch_bounds__(32 * NY_WARPS)
   while (top > 0) {
     const NyTri T = st[--top];
     __syncwarp();
-    double yA[3], yB[3], yC[3], yG[3];
-    ny_map(P, T.a0, T.a1, yA, nullptr, nullptr);
-    ny_map(P, T.b0, T.b1, yB, nullptr, nullptr);
-    ny_map(P, T.c0, T.c1, yC, nullptr, nullptr);
-    ny_map(P, (T.a0 + T.b0 + T.c0) / 3.0, (T.a1 + T.b1 + T.c1) / 3.0, yG, nullptr, nullptr);
-    const double h = fmax(ny_dist(yA, yB), fmax(ny_dist(yB, yC), ny_dist(yC, yA)));
-    const double d = fmin(fmin(ny_dist(x, yA), ny_dist(x, yB)), fmin(ny_dist(x, yC), ny_dist(x, yG)));
+    // lane & 3 selects one of the corners A, B, C or the centroid G: one map per lane instead of four, the
+    // distances combined by shuffles inside each group of four lanes (every group holds the same values, so the
+    // decision stays uniform over the warp)
+    const int sel = lane & 3;
+    const double pa = sel == 0 ? T.a0 : sel == 1 ? T.b0 : sel == 2 ? T.c0 : (T.a0 + T.b0 + T.c0) / 3.0;
+    const double pb = sel == 0 ? T.a1 : sel == 1 ? T.b1 : sel == 2 ? T.c1 : (T.a1 + T.b1 + T.c1) / 3.0;
+    double ys[3], yn[3];
+    ny_map(P, pa, pb, ys, nullptr, nullptr);
+    const int nxt = (lane & ~3) | (sel == 2 ? 0 : sel + 1);  // A -> B -> C -> A (G: unused)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) yn[c] = __shfl_sync(0xffffffffu, ys[c], nxt);
+    double h = sel == 3 ? 0.0 : ny_dist(ys, yn);
+    double d = ny_dist(x, ys);
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+      d = fmin(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
     if (h > theta * d && T.depth < max_depth) {
       if (lane == 0) {
         const double ab0 = 0.5 * (T.a0 + T.b0), ab1 = 0.5 * (T.a1 + T.b1);
@@ -176,7 +195,7 @@ __global__ void __launch_bounds__(32 * NY_WARPS)
     }
   if (touching) {
     if (lane == 0) atomicOr(flag, 2);
-    return;
+    continue;
   }
   if (lane < 6) {
     double2 w = make_double2(0.0, 0.0);
@@ -191,6 +210,8 @@ __global__ void __launch_bounds__(32 * NY_WARPS)
       delta[6 * p + lane] = make_double2(w.x - wj * kv.x, w.y - wj * kv.y);
     }
   }
+  __syncwarp();
+  }  // next pair
 }
 
 // Gauss-Legendre nodes and weights on [0, 1] (Newton iteration on P_n from the Chebyshev-like initial guess)
@@ -325,7 +346,7 @@ extern "C" fda_status fda_nystrom_weights(int kernel, double k, double alpha_re,
   const size_t obytes = (size_t)npairs * 6 * sizeof(double2);
   double2 *dw = nullptr, *dd = nullptr;
   void *ow = nullptr, *od = nullptr;
-  int* dflag = nullptr;
+  int* dflag = nullptr;  // flag word, then the 8-byte pair counter
   auto cleanup = [&] {
     if (ow) cudaFree(ow);
     if (od) cudaFree(od);
@@ -353,15 +374,20 @@ extern "C" fda_status fda_nystrom_weights(int kernel, double k, double alpha_re,
     else
       dd = static_cast<double2*>(od);
   }
-  if ((e = cudaMalloc(&dflag, sizeof(int))) != cudaSuccess) return fail(e);
-  if ((e = cudaMemset(dflag, 0, sizeof(int))) != cudaSuccess) return fail(e);
-  const unsigned grid = (unsigned)((npairs + NY_WARPS - 1) / NY_WARPS);
+  if ((e = cudaMalloc(&dflag, 16)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(dflag, 0, 16)) != cudaSuccess) return fail(e);
+  unsigned long long* dnext = reinterpret_cast<unsigned long long*>(dflag + 2);
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // persistent grid: the resident CTAs of every SM (launch bounds: 4 per SM), never more CTAs than pairs
+  const unsigned grid = (unsigned)std::min<int64_t>((npairs + NY_WARPS - 1) / NY_WARPS, (int64_t)std::max(1, nsm) * 4);
   const double2 alpha = make_double2(alpha_re, alpha_im);
   auto launch = [&](auto kern) {
     kern<<<grid, 32 * NY_WARPS>>>(static_cast<const double*>(de.ptr), ne, static_cast<const double*>(dx.ptr),
                                   static_cast<const double*>(dn.ptr), nt, static_cast<const int64_t*>(dt.ptr),
                                   static_cast<const int64_t*>(dpe.ptr), npairs, k, alpha, nq, theta, max_depth, dw, dd,
-                                  dflag);
+                                  dflag, dnext);
   };
   if (kernel == FDA_KERNEL_BMH)
     launch(k_nystrom_weights<FDA_KERNEL_BMH>);

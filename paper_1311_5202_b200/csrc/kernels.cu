@@ -964,13 +964,6 @@ static void gt_cfg(const GTrans& T, int* p, int* nbuf, bool* stage) {
       if (cl[i][0] == a && cl[i][1] == b && cl[i][2] == c) return i;
     return -1;
   }();
-  // FDA_GT_DB16=1 (experiment): 16 columns, double-buffered gather and the operator staged, when two such CTAs
-  // fit an SM (the HF -> HF transitions: ncu shows the single-buffered gather wait as their top stall)
-  static const bool db16 = getenv("FDA_GT_DB16") && getenv("FDA_GT_DB16")[0] == '1';
-  if (db16 && allow && gt_smem(T, 16, 2, true) <= budget) {
-    *p = 16, *nbuf = 2, *stage = true;
-    return;
-  }
   int ci = 0;
   for (auto& c : cand) {
     if (ci++ < force) continue;
@@ -1111,7 +1104,6 @@ cudaError_t launch_gtrans(const GTrans& T, const double2* X, double2* Y, cudaStr
   if (p == 32 && nb == 1 && stg) return gt_launch<32, 1, true>(T, X, Y, sm, st);
   if (p == 32 && nb == 2) return gt_launch<32, 2, false>(T, X, Y, sm, st);
   if (p == 32) return gt_launch<32, 1, false>(T, X, Y, sm, st);
-  if (p == 16 && nb == 2 && stg) return gt_launch<16, 2, true>(T, X, Y, sm, st);
   if (p == 16 && stg) return gt_launch<16, 1, true>(T, X, Y, sm, st);
   if (p == 16 && nb == 2) return gt_launch<16, 2, false>(T, X, Y, sm, st);
   if (p == 16) return gt_launch<16, 1, false>(T, X, Y, sm, st);

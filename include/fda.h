@@ -228,7 +228,7 @@ fda_status fda_plan_export_exchange(fda_plan plan, int peer, int recv, int64_t* 
  *                 xi1, xi2 >= 0, xi1 + xi2 <= 1, and 6 reference weights (sum 1/2; w_j = wref_j J(xi_j))
  *   tx, tn        nt x 3 field points and their unit normals
  *   pair_t/pair_e npairs indices into tx / elem_nodes (int64)
- *   nq, theta, max_depth   0 selects the defaults 8, 0.5, 16; limits nq <= 16, theta in (0, 1], max_depth <= 20
+ *   nq, theta, max_depth   0 selects the defaults 12, 0.5, 16; limits nq <= 16, theta in (0, 1], max_depth <= 20
  *   wbar          npairs x 6 complex128 (12 doubles per pair), the weights; may be NULL
  *   delta         npairs x 6 complex128, wbar_j - w_j K(x_t, y_j): the value the correction CSR of
  *                 fda_plan_set_correction holds for (row t, column of node j of e); may be NULL (not both)

@@ -138,6 +138,28 @@ def test_edge_cases():
     assert abs(w6.sum() - (-omega / (4 * np.pi))) <= 1e-10    # sum_j wbar_j = I_0 (phi^(0) = 1)
 
 
+def test_anisotropic_mesh_pairs():
+    """Prolate spheroid 10:1:1 (the geometry of config 4, coarse): stretched elements, larger local regions."""
+    fda = _fda()
+    nodes = synth.spheroid(10.0, 1.0, 0.5)
+    x, n, w, hmax, samples = synth.quadrature_cloud(nodes)
+    ptr, idx = synth.local_regions(samples, hmax, x)
+    xi, wref = _rule()
+    ts, es = [], []
+    for t in range(1, x.shape[0], 9):
+        for e in idx[ptr[t]:ptr[t + 1]]:
+            if e != t // 6:
+                ts.append(t), es.append(int(e))
+    ts, es = np.array(ts, np.int64), np.array(es, np.int64)
+    k = 4.0
+    wbar = np.zeros((ts.shape[0], 6), np.complex128)
+    fda.fda_nystrom_weights(fda.FDA_KERNEL_BMH, k, 1j / k, nodes, xi, wref, x, n, ts, es, wbar)
+    ref = oracle.corrected_weights(oracle.KIND_BMH, nodes, xi, x, n, ts, es, k, 1j / k)
+    err = _pair_err(wbar, ref)
+    print(f"spheroid: {ts.shape[0]} pairs, max pair error {err:.2e}")
+    assert err <= 1e-10
+
+
 def test_corrected_rows_feed_the_apply():
     """The delta values fill the D_i pattern of the correction CSR (self elements left zero: [rjj_int] is out of
     scope) and the apply with them matches the oracle's rows built from the oracle's own weights."""

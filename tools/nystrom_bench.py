@@ -46,7 +46,7 @@ def main():
         times.append(time.perf_counter() - t0)
     t = min(times[1:])
     print(json.dumps({"config": a.config, "N": p.N, "pairs": int(ts.shape[0]), "pairs_per_point": ts.shape[0] / p.N,
-                      "ms": 1e3 * t, "Mpairs_per_s": ts.shape[0] / t / 1e6, "nq": a.nq or 8, "theta": a.theta or 0.5,
+                      "ms": 1e3 * t, "Mpairs_per_s": ts.shape[0] / t / 1e6, "nq": a.nq or 12, "theta": a.theta or 0.5,
                       "checksum": float(out.abs().sum().item())}))
 
 

@@ -6,8 +6,10 @@
 // and the moments I_n, nearly singular when x is close to Delta, are computed "by using a recursive subdivision
 // quadrature".  The paper gives neither the subdivision criterion nor the rule; reading R27
 // (DESIGN.md): a sub-triangle of the reference triangle is split at its edge mid-points while its largest mapped
-// edge exceeds theta x the distance from x to the nearest of its mapped corners and centroid; a leaf is
-// integrated by the nq x nq Gauss-Legendre product rule on the collapsed square.
+// edge h exceeds theta x the distance from x to the nearest of its mapped corners and centroid, or while the map
+// is not flat enough on it (|y(G) - mean of the mapped corners| > gamma h: strongly curved elements, where the
+// element map rather than the distance limits the smoothness of the integrand); a leaf is integrated by the
+// nq x nq Gauss-Legendre product rule on the collapsed square.
 //
 // One warp per (field point, element) pair: the subdivision is an explicit depth-first stack in shared memory
 // (every lane takes the same decisions), the nq^2 points of a leaf are spread over the lanes, the six complex
@@ -97,8 +99,8 @@ __global__ void __launch_bounds__(32 * NY_WARPS, 4)
     k_nystrom_weights(const double* __restrict__ elem, int64_t ne, const double* __restrict__ tx,
                       const double* __restrict__ tn, int64_t nt, const int64_t* __restrict__ pair_t,
                       const int64_t* __restrict__ pair_e, int64_t npairs, double k, double2 alpha, int nq,
-                      double theta, int max_depth, double2* __restrict__ wbar, double2* __restrict__ delta,
-                      int* __restrict__ flag, unsigned long long* __restrict__ next) {
+                      double theta, double gamma, int max_depth, double2* __restrict__ wbar,
+                      double2* __restrict__ delta, int* __restrict__ flag, unsigned long long* __restrict__ next) {
   __shared__ NyTri stack[NY_WARPS][NY_STACK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Persistent warps take pairs from a device counter: the work per pair varies by two orders of magnitude
@@ -147,12 +149,21 @@ __global__ void __launch_bounds__(32 * NY_WARPS, 4)
     for (int c = 0; c < 3; ++c) yn[c] = __shfl_sync(0xffffffffu, ys[c], nxt);
     double h = sel == 3 ? 0.0 : ny_dist(ys, yn);
     double d = ny_dist(x, ys);
+    // flatness of the mapped sub-triangle: |y(G) - (y(A) + y(B) + y(C)) / 3|, the quadratic part of the map
+    double cs[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cs[c] = sel == 3 ? 0.0 : ys[c];
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
       h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
       d = fmin(d, __shfl_xor_sync(0xffffffffu, d, o));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cs[c] += __shfl_xor_sync(0xffffffffu, cs[c], o);
     }
-    if (h > theta * d && T.depth < max_depth) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cs[c] *= (1.0 / 3.0);
+    const double flat = __shfl_sync(0xffffffffu, ny_dist(ys, cs), lane | 3);
+    if ((h > theta * d || flat > gamma * h) && T.depth < max_depth) {
       if (lane == 0) {
         const double ab0 = 0.5 * (T.a0 + T.b0), ab1 = 0.5 * (T.a1 + T.b1);
         const double bc0 = 0.5 * (T.b0 + T.c0), bc1 = 0.5 * (T.b1 + T.c1);
@@ -298,16 +309,19 @@ struct DevIn {
 extern "C" fda_status fda_nystrom_weights(int kernel, double k, double alpha_re, double alpha_im,
                                           const double* elem_nodes, int64_t ne, const double* xi, const double* wref,
                                           const double* tx, const double* tn, int64_t nt, const int64_t* pair_t,
-                                          const int64_t* pair_e, int64_t npairs, int nq, double theta, int max_depth,
-                                          double* wbar, double* delta) {
+                                          const int64_t* pair_e, int64_t npairs, int nq, double theta, double gamma,
+                                          int max_depth, double* wbar, double* delta) {
   using namespace fda;
   if (kernel != FDA_KERNEL_BMH && kernel != FDA_KERNEL_BMG && kernel != FDA_KERNEL_T1) return FDA_ERR_INVALID_ARG;
   if (!(k >= 0.0) || !std::isfinite(k) || !std::isfinite(alpha_re) || !std::isfinite(alpha_im)) return FDA_ERR_INVALID_ARG;
   if (ne < 0 || nt < 0 || npairs < 0 || !xi || !wref || (!wbar && !delta)) return FDA_ERR_INVALID_ARG;
-  if (nq == 0) nq = 12;  // 8 reaches 5e-13 on gently curved elements but only 8e-7 on the tip elements of a 10:1:1 spheroid (R27)
+  if (nq == 0) nq = 8;
+  // without the flatness split, nq = 8 reaches 5e-13 on gently curved elements but only 8e-7 on the tip
+  // elements of a 10:1:1 spheroid, where the element map, not the distance, limits the smoothness (R27)
+  if (gamma == 0.0) gamma = 0.05;
   if (theta == 0.0) theta = 0.5;
   if (max_depth == 0) max_depth = 16;
-  if (nq < 2 || nq > NY_MAXQ || !(theta > 0.0 && theta <= 1.0) || max_depth < 1 || max_depth > NY_MAXDEPTH)
+  if (nq < 2 || nq > NY_MAXQ || !(theta > 0.0 && theta <= 1.0) || !(gamma > 0.0) || max_depth < 1 || max_depth > NY_MAXDEPTH)
     return FDA_ERR_INVALID_ARG;
   if (npairs == 0) return FDA_OK;
   if (!elem_nodes || !tx || !tn || !pair_t || !pair_e || ne == 0 || nt == 0) return FDA_ERR_INVALID_ARG;
@@ -386,8 +400,8 @@ extern "C" fda_status fda_nystrom_weights(int kernel, double k, double alpha_re,
   auto launch = [&](auto kern) {
     kern<<<grid, 32 * NY_WARPS>>>(static_cast<const double*>(de.ptr), ne, static_cast<const double*>(dx.ptr),
                                   static_cast<const double*>(dn.ptr), nt, static_cast<const int64_t*>(dt.ptr),
-                                  static_cast<const int64_t*>(dpe.ptr), npairs, k, alpha, nq, theta, max_depth, dw, dd,
-                                  dflag, dnext);
+                                  static_cast<const int64_t*>(dpe.ptr), npairs, k, alpha, nq, theta, gamma, max_depth, dw,
+                                  dd, dflag, dnext);
   };
   if (kernel == FDA_KERNEL_BMH)
     launch(k_nystrom_weights<FDA_KERNEL_BMH>);

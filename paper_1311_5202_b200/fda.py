@@ -91,7 +91,8 @@ _lib.fda_apply_up.argtypes = [_P, _P, _P]
 _lib.fda_apply_down.argtypes = [_P, _P, _P]
 _lib.fda_plan_export_exchange.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_I64), _P, _P, _P]
 _lib.fda_nystrom_weights.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _I64, _P, _P,
-                                     _P, _P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_double, ctypes.c_int, _P, _P]
+                                     _P, _P, _I64, _P, _P, _I64, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, _P,
+                                     _P]
 
 
 class FDAError(RuntimeError):
@@ -258,7 +259,7 @@ def fda_plan_export_exchange(plan, peer: int, recv: bool):
 
 
 def fda_nystrom_weights(kernel, k, alpha, elem_nodes, xi, wref, tx, tn, pair_t, pair_e, wbar=None, delta=None,
-                        nq=0, theta=0.0, max_depth=0):
+                        nq=0, theta=0.0, gamma=0.0, max_depth=0):
     """Locally corrected weights of (field point, element) pairs (include/fda.h).  elem_nodes (ne, 6, 3),
     xi (6, 2), wref (6), tx / tn (nt, 3), pair_t / pair_e int64 (npairs); wbar / delta (npairs, 6) complex128,
     filled in place (numpy arrays or torch tensors, host or device)."""
@@ -268,7 +269,8 @@ def fda_nystrom_weights(kernel, k, alpha, elem_nodes, xi, wref, tx, tn, pair_t, 
     npairs = int(pair_t.shape[0])
     _check(_lib.fda_nystrom_weights(int(kernel), float(k), alpha.real, alpha.imag, _ptr(elem_nodes), ne, _ptr(xi),
                                     _ptr(wref), _ptr(tx), _ptr(tn), nt, _ptr(pair_t), _ptr(pair_e), npairs, int(nq),
-                                    float(theta), int(max_depth), _ptr(wbar), _ptr(delta)), "fda_nystrom_weights")
+                                    float(theta), float(gamma), int(max_depth), _ptr(wbar), _ptr(delta)),
+           "fda_nystrom_weights")
 
 
 def fda_plan_destroy(plan):

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--theta", type=float, default=0.0)
+    ap.add_argument("--gamma", type=float, default=0.0)
     a = ap.parse_args()
     p = synth.make_problem(a.config)
     ptr, idx = synth.local_regions(p.samples, p.hmax, p.x)
@@ -41,12 +42,12 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         fda.fda_nystrom_weights(fda.FDA_KERNEL_BMH, p.k, p.alpha, d["nodes"], d["xi"], d["wref"], d["x"], d["n"],
-                                d["ts"], d["es"], out, dl, nq=a.nq, theta=a.theta)
+                                d["ts"], d["es"], out, dl, nq=a.nq, theta=a.theta, gamma=a.gamma)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     t = min(times[1:])
     print(json.dumps({"config": a.config, "N": p.N, "pairs": int(ts.shape[0]), "pairs_per_point": ts.shape[0] / p.N,
-                      "ms": 1e3 * t, "Mpairs_per_s": ts.shape[0] / t / 1e6, "nq": a.nq or 12, "theta": a.theta or 0.5,
+                      "ms": 1e3 * t, "Mpairs_per_s": ts.shape[0] / t / 1e6, "nq": a.nq or 8, "gamma": a.gamma or 0.05, "theta": a.theta or 0.5,
                       "checksum": float(out.abs().sum().item())}))
 
 

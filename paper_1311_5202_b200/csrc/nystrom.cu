@@ -39,29 +39,33 @@ struct NyConst {
 };
 __constant__ NyConst c_ny;
 
-// y(xi), and optionally the unit normal t1 x t2 / J and J, of the 6-node triangle P (corners 1 2 3, mid-edges
-// 12 23 31)
-__device__ __forceinline__ void ny_map(const double (&P)[18], double a, double b, double (&y)[3], double* nv,
-                                       double* J) {
-  const double l1 = 1.0 - a - b;
-  const double N[6] = {l1 * (2 * l1 - 1), a * (2 * a - 1), b * (2 * b - 1), 4 * l1 * a, 4 * a * b, 4 * b * l1};
+// The 6-node triangle (corners 1 2 3, mid-edges 12 23 31) as a quadratic polynomial in (a, b):
+//   y = c0 + c1 a + c2 b + c3 a^2 + c4 a b + c5 b^2   (the shape functions N_q(a, b) expanded in monomials)
+__device__ __forceinline__ void ny_coeffs(const double* __restrict__ P, double (&C)[18]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) s = fma(N[q], P[3 * q + c], s);
-    y[c] = s;
+    const double p1 = P[c], p2 = P[3 + c], p3 = P[6 + c], p4 = P[9 + c], p5 = P[12 + c], p6 = P[15 + c];
+    C[c] = p1;
+    C[3 + c] = -3.0 * p1 - p2 + 4.0 * p4;
+    C[6 + c] = -3.0 * p1 - p3 + 4.0 * p6;
+    C[9 + c] = 2.0 * p1 + 2.0 * p2 - 4.0 * p4;
+    C[12 + c] = 4.0 * (p1 - p4 + p5 - p6);
+    C[15 + c] = 2.0 * p1 + 2.0 * p3 - 4.0 * p6;
   }
+}
+// y(a, b), and optionally the unit normal t1 x t2 / J and J (t1 = dy/da, t2 = dy/db)
+__device__ __forceinline__ void ny_map(const double (&C)[18], double a, double b, double (&y)[3], double* nv,
+                                       double* J) {
+  const double aa = a * a, ab = a * b, bb = b * b;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    y[c] = fma(C[15 + c], bb, fma(C[12 + c], ab, fma(C[9 + c], aa, fma(C[6 + c], b, fma(C[3 + c], a, C[c])))));
   if (nv) {
-    const double d1[6] = {1 - 4 * l1, 4 * a - 1, 0.0, 4 * (l1 - a), 4 * b, -4 * b};
-    const double d2[6] = {1 - 4 * l1, 0.0, 4 * b - 1, -4 * a, 4 * a, 4 * (l1 - b)};
     double t1[3], t2[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) s1 = fma(d1[q], P[3 * q + c], s1), s2 = fma(d2[q], P[3 * q + c], s2);
-      t1[c] = s1, t2[c] = s2;
+      t1[c] = fma(2.0 * C[9 + c], a, fma(C[12 + c], b, C[3 + c]));
+      t2[c] = fma(2.0 * C[15 + c], b, fma(C[12 + c], a, C[6 + c]));
     }
     const double cx = t1[1] * t2[2] - t1[2] * t2[1], cy = t1[2] * t2[0] - t1[0] * t2[2],
                  cz = t1[0] * t2[1] - t1[1] * t2[0];
@@ -117,9 +121,8 @@ __global__ void __launch_bounds__(32 * NY_WARPS, 4)
     if (lane == 0) atomicOr(flag, 1);
     continue;
   }
-  double P[18], x[3], nx[3];
-#pragma unroll
-  for (int i = 0; i < 18; ++i) P[i] = elem[18 * e + i];
+  double P[18], x[3], nx[3];  // P: the element's monomial coefficients
+  ny_coeffs(elem + 18 * e, P);
 #pragma unroll
   for (int c = 0; c < 3; ++c) x[c] = tx[3 * t + c], nx[c] = tn[3 * t + c];
 

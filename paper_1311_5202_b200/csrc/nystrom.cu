@@ -112,119 +112,119 @@ __global__ void __launch_bounds__(32 * NY_WARPS, 4)
   // pair -> warp map leaves most resident warps idle (ncu: 6.6 of 64 warps active per SM, 26 Mpairs/s).
   // The result of a pair does not depend on which warp computes it.
   for (;;) {
-  long long p = 0;
-  if (lane == 0) p = (long long)atomicAdd(next, 1ull);
-  p = __shfl_sync(0xffffffffu, p, 0);
-  if (p >= npairs) return;
-  const int64_t t = pair_t[p], e = pair_e[p];
-  if (t < 0 || t >= nt || e < 0 || e >= ne) {
-    if (lane == 0) atomicOr(flag, 1);
-    continue;
-  }
-  double P[18], x[3], nx[3];  // P: the element's monomial coefficients
-  ny_coeffs(elem + 18 * e, P);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) x[c] = tx[3 * t + c], nx[c] = tn[3 * t + c];
-
-  double2 mom[6];
-#pragma unroll
-  for (int n = 0; n < 6; ++n) mom[n] = make_double2(0.0, 0.0);
-  NyTri* st = stack[warp];
-  int top = 0;
-  if (lane == 0) st[0] = NyTri{0.0, 0.0, 1.0, 0.0, 0.0, 1.0, 0};
-  __syncwarp();
-  top = 1;
-  bool touching = false;
-  const int nq2 = nq * nq;
-  while (top > 0) {
-    const NyTri T = st[--top];
-    __syncwarp();
-    // lane & 3 selects one of the corners A, B, C or the centroid G: one map per lane instead of four, the
-    // distances combined by shuffles inside each group of four lanes (every group holds the same values, so the
-    // decision stays uniform over the warp)
-    const int sel = lane & 3;
-    const double pa = sel == 0 ? T.a0 : sel == 1 ? T.b0 : sel == 2 ? T.c0 : (T.a0 + T.b0 + T.c0) / 3.0;
-    const double pb = sel == 0 ? T.a1 : sel == 1 ? T.b1 : sel == 2 ? T.c1 : (T.a1 + T.b1 + T.c1) / 3.0;
-    double ys[3], yn[3];
-    ny_map(P, pa, pb, ys, nullptr, nullptr);
-    const int nxt = (lane & ~3) | (sel == 2 ? 0 : sel + 1);  // A -> B -> C -> A (G: unused)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) yn[c] = __shfl_sync(0xffffffffu, ys[c], nxt);
-    double h = sel == 3 ? 0.0 : ny_dist(ys, yn);
-    double d = ny_dist(x, ys);
-    // flatness of the mapped sub-triangle: |y(G) - (y(A) + y(B) + y(C)) / 3|, the quadratic part of the map
-    double cs[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) cs[c] = sel == 3 ? 0.0 : ys[c];
-#pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
-      d = fmin(d, __shfl_xor_sync(0xffffffffu, d, o));
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cs[c] += __shfl_xor_sync(0xffffffffu, cs[c], o);
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) cs[c] *= (1.0 / 3.0);
-    const double flat = __shfl_sync(0xffffffffu, ny_dist(ys, cs), lane | 3);
-    if ((h > theta * d || flat > gamma * h) && T.depth < max_depth) {
-      if (lane == 0) {
-        const double ab0 = 0.5 * (T.a0 + T.b0), ab1 = 0.5 * (T.a1 + T.b1);
-        const double bc0 = 0.5 * (T.b0 + T.c0), bc1 = 0.5 * (T.b1 + T.c1);
-        const double ca0 = 0.5 * (T.c0 + T.a0), ca1 = 0.5 * (T.c1 + T.a1);
-        const int dd = T.depth + 1;
-        st[top + 0] = NyTri{ab0, ab1, bc0, bc1, ca0, ca1, dd};
-        st[top + 1] = NyTri{ca0, ca1, bc0, bc1, T.c0, T.c1, dd};
-        st[top + 2] = NyTri{ab0, ab1, T.b0, T.b1, bc0, bc1, dd};
-        st[top + 3] = NyTri{T.a0, T.a1, ab0, ab1, ca0, ca1, dd};
-      }
-      top += 4;
-      __syncwarp();
+    long long p = 0;
+    if (lane == 0) p = (long long)atomicAdd(next, 1ull);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= npairs) return;
+    const int64_t t = pair_t[p], e = pair_e[p];
+    if (t < 0 || t >= nt || e < 0 || e >= ne) {
+      if (lane == 0) atomicOr(flag, 1);
       continue;
     }
-    // still unresolved at the deepest level: the field point lies on the element (or closer to it than
-    // 2^-max_depth side lengths / theta) -- the singular case this routine does not cover
-    if (!(h <= theta * d)) touching = true;
-    const double area2 = fabs((T.b0 - T.a0) * (T.c1 - T.a1) - (T.b1 - T.a1) * (T.c0 - T.a0));
-    for (int q = lane; q < nq2; q += 32) {
-      const int ia = q / nq, ib = q - ia * nq;
-      const double u = c_ny.gu[ia], v = c_ny.gu[ib];
-      const double s1 = T.a0 + u * ((T.b0 - T.a0) + v * (T.c0 - T.b0));
-      const double s2 = T.a1 + u * ((T.b1 - T.a1) + v * (T.c1 - T.b1));
-      double y[3], nyv[3], J;
-      ny_map(P, s1, s2, y, nyv, &J);
-      const double2 kv = ny_kernel<KERNEL>(x, nx, y, nyv, k, alpha);
-      const double wq = c_ny.gw[ia] * c_ny.gw[ib] * u * area2 * J;
-      const double2 f = make_double2(kv.x * wq, kv.y * wq);
-      const double m[6] = {1.0, s1, s2, s1 * s1, s1 * s2, s2 * s2};
+    double P[18], x[3], nx[3];  // P: the element's monomial coefficients
+    ny_coeffs(elem + 18 * e, P);
 #pragma unroll
-      for (int n = 0; n < 6; ++n) mom[n].x = fma(f.x, m[n], mom[n].x), mom[n].y = fma(f.y, m[n], mom[n].y);
+    for (int c = 0; c < 3; ++c) x[c] = tx[3 * t + c], nx[c] = tn[3 * t + c];
+
+    double2 mom[6];
+#pragma unroll
+    for (int n = 0; n < 6; ++n) mom[n] = make_double2(0.0, 0.0);
+    NyTri* st = stack[warp];
+    int top = 0;
+    if (lane == 0) st[0] = NyTri{0.0, 0.0, 1.0, 0.0, 0.0, 1.0, 0};
+    __syncwarp();
+    top = 1;
+    bool touching = false;
+    const int nq2 = nq * nq;
+    while (top > 0) {
+      const NyTri T = st[--top];
+      __syncwarp();
+      // lane & 3 selects one of the corners A, B, C or the centroid G: one map per lane instead of four, the
+      // distances combined by shuffles inside each group of four lanes (every group holds the same values, so the
+      // decision stays uniform over the warp)
+      const int sel = lane & 3;
+      const double pa = sel == 0 ? T.a0 : sel == 1 ? T.b0 : sel == 2 ? T.c0 : (T.a0 + T.b0 + T.c0) / 3.0;
+      const double pb = sel == 0 ? T.a1 : sel == 1 ? T.b1 : sel == 2 ? T.c1 : (T.a1 + T.b1 + T.c1) / 3.0;
+      double ys[3], yn[3];
+      ny_map(P, pa, pb, ys, nullptr, nullptr);
+      const int nxt = (lane & ~3) | (sel == 2 ? 0 : sel + 1);  // A -> B -> C -> A (G: unused)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) yn[c] = __shfl_sync(0xffffffffu, ys[c], nxt);
+      double h = sel == 3 ? 0.0 : ny_dist(ys, yn);
+      double d = ny_dist(x, ys);
+      // flatness of the mapped sub-triangle: |y(G) - (y(A) + y(B) + y(C)) / 3|, the quadratic part of the map
+      double cs[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cs[c] = sel == 3 ? 0.0 : ys[c];
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+        d = fmin(d, __shfl_xor_sync(0xffffffffu, d, o));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cs[c] += __shfl_xor_sync(0xffffffffu, cs[c], o);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cs[c] *= (1.0 / 3.0);
+      const double flat = __shfl_sync(0xffffffffu, ny_dist(ys, cs), lane | 3);
+      if ((h > theta * d || flat > gamma * h) && T.depth < max_depth) {
+        if (lane == 0) {
+          const double ab0 = 0.5 * (T.a0 + T.b0), ab1 = 0.5 * (T.a1 + T.b1);
+          const double bc0 = 0.5 * (T.b0 + T.c0), bc1 = 0.5 * (T.b1 + T.c1);
+          const double ca0 = 0.5 * (T.c0 + T.a0), ca1 = 0.5 * (T.c1 + T.a1);
+          const int dd = T.depth + 1;
+          st[top + 0] = NyTri{ab0, ab1, bc0, bc1, ca0, ca1, dd};
+          st[top + 1] = NyTri{ca0, ca1, bc0, bc1, T.c0, T.c1, dd};
+          st[top + 2] = NyTri{ab0, ab1, T.b0, T.b1, bc0, bc1, dd};
+          st[top + 3] = NyTri{T.a0, T.a1, ab0, ab1, ca0, ca1, dd};
+        }
+        top += 4;
+        __syncwarp();
+        continue;
+      }
+      // still unresolved at the deepest level: the field point lies on the element (or closer to it than
+      // 2^-max_depth side lengths / theta) -- the singular case this routine does not cover
+      if (!(h <= theta * d)) touching = true;
+      const double area2 = fabs((T.b0 - T.a0) * (T.c1 - T.a1) - (T.b1 - T.a1) * (T.c0 - T.a0));
+      for (int q = lane; q < nq2; q += 32) {
+        const int ia = q / nq, ib = q - ia * nq;
+        const double u = c_ny.gu[ia], v = c_ny.gu[ib];
+        const double s1 = T.a0 + u * ((T.b0 - T.a0) + v * (T.c0 - T.b0));
+        const double s2 = T.a1 + u * ((T.b1 - T.a1) + v * (T.c1 - T.b1));
+        double y[3], nyv[3], J;
+        ny_map(P, s1, s2, y, nyv, &J);
+        const double2 kv = ny_kernel<KERNEL>(x, nx, y, nyv, k, alpha);
+        const double wq = c_ny.gw[ia] * c_ny.gw[ib] * u * area2 * J;
+        const double2 f = make_double2(kv.x * wq, kv.y * wq);
+        const double m[6] = {1.0, s1, s2, s1 * s1, s1 * s2, s2 * s2};
+#pragma unroll
+        for (int n = 0; n < 6; ++n) mom[n].x = fma(f.x, m[n], mom[n].x), mom[n].y = fma(f.y, m[n], mom[n].y);
+      }
     }
-  }
 #pragma unroll
-  for (int n = 0; n < 6; ++n)
+    for (int n = 0; n < 6; ++n)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mom[n].x += __shfl_xor_sync(0xffffffffu, mom[n].x, o);
-      mom[n].y += __shfl_xor_sync(0xffffffffu, mom[n].y, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        mom[n].x += __shfl_xor_sync(0xffffffffu, mom[n].x, o);
+        mom[n].y += __shfl_xor_sync(0xffffffffu, mom[n].y, o);
+      }
+    if (touching) {
+      if (lane == 0) atomicOr(flag, 2);
+      continue;
     }
-  if (touching) {
-    if (lane == 0) atomicOr(flag, 2);
-    continue;
-  }
-  if (lane < 6) {
-    double2 w = make_double2(0.0, 0.0);
+    if (lane < 6) {
+      double2 w = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int n = 0; n < 6; ++n) w.x = fma(c_ny.minv[lane][n], mom[n].x, w.x), w.y = fma(c_ny.minv[lane][n], mom[n].y, w.y);
-    if (wbar) wbar[6 * p + lane] = w;
-    if (delta) {  // wbar_j - w_j K(x, y_j): what the correction CSR holds next to the plain far quadrature (R4)
-      double y[3], nyv[3], J;
-      ny_map(P, c_ny.xi[lane][0], c_ny.xi[lane][1], y, nyv, &J);
-      const double2 kv = ny_kernel<KERNEL>(x, nx, y, nyv, k, alpha);
-      const double wj = c_ny.wref[lane] * J;
-      delta[6 * p + lane] = make_double2(w.x - wj * kv.x, w.y - wj * kv.y);
+      for (int n = 0; n < 6; ++n) w.x = fma(c_ny.minv[lane][n], mom[n].x, w.x), w.y = fma(c_ny.minv[lane][n], mom[n].y, w.y);
+      if (wbar) wbar[6 * p + lane] = w;
+      if (delta) {  // wbar_j - w_j K(x, y_j): what the correction CSR holds next to the plain far quadrature (R4)
+        double y[3], nyv[3], J;
+        ny_map(P, c_ny.xi[lane][0], c_ny.xi[lane][1], y, nyv, &J);
+        const double2 kv = ny_kernel<KERNEL>(x, nx, y, nyv, k, alpha);
+        const double wj = c_ny.wref[lane] * J;
+        delta[6 * p + lane] = make_double2(w.x - wj * kv.x, w.y - wj * kv.y);
+      }
     }
-  }
-  __syncwarp();
+    __syncwarp();
   }  // next pair
 }
 

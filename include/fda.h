@@ -234,7 +234,8 @@ fda_status fda_plan_export_exchange(fda_plan plan, int peer, int recv, int64_t* 
  *   wbar          npairs x 6 complex128 (12 doubles per pair), the weights; may be NULL
  *   delta         npairs x 6 complex128, wbar_j - w_j K(x_t, y_j): the value the correction CSR of
  *                 fda_plan_set_correction holds for (row t, column of node j of e); may be NULL (not both)
- * Arrays may be host or device memory; the call synchronises.  Errors: FDA_ERR_INVALID_ARG (arguments, an index
+ * Arrays may be host or device memory; the call runs on the default stream and synchronises (concurrent calls are
+ * serialised).  Errors: FDA_ERR_INVALID_ARG (arguments, an index
  * out of range, a field point on its element), FDA_ERR_CUDA (no device / CUDA error), FDA_ERR_OOM. */
 fda_status fda_nystrom_weights(int kernel, double k, double alpha_re, double alpha_im, const double* elem_nodes,
                                int64_t ne, const double* xi, const double* wref, const double* tx, const double* tn,

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "fda.h"
@@ -333,6 +334,9 @@ extern "C" fda_status fda_nystrom_weights(int kernel, double k, double alpha_re,
     cudaGetLastError();
     return FDA_ERR_CUDA;  // no CPU fallback
   }
+  // the rule constants live in one __constant__ block: concurrent calls are serialised
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   NyConst C{};
   gauss_legendre01(nq, C.gu, C.gw);
   double hxi[12], hw[6];

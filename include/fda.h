@@ -112,6 +112,10 @@ typedef struct {
   int32_t graph;           /* 1 (default): fda_apply replays a CUDA graph of its device-resident middle (near field,
                               upward pass, M2L, L2L, L2T; captured on the second apply of a phase mask, single-rank
                               plans; fda_plan_set_correction drops it); 0 (or env FDA_GRAPH=0): plain launches */
+  int32_t deterministic;   /* 1: bit-reproducible applies -- every translation runs as owned items (an item owns its
+                              output slots: plain read-modify-write in a fixed order instead of FP64 reductions) and
+                              the P2P one-sided; equal to the default apply to rounding (3e-16) and 2.6x slower at
+                              config 5 (565 vs 218 ms); default 0 */
 } fda_options;
 
 typedef struct {

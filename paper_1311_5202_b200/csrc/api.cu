@@ -107,6 +107,7 @@ struct fda_plan_s {
   // phase mask on the plan's capture stream, replayed on the caller's stream between the permute and the
   // unpermute (which take the caller's pointers).  fda_options.graph / FDA_GRAPH; single-rank plans.
   bool graph_on = false;
+  bool deterministic = false;  // fda_options.deterministic: owned items everywhere, one-sided P2P
   cudaStream_t gstream = nullptr;
   std::map<uint32_t, cudaGraphExec_t> gexec;
   std::map<uint32_t, int> gcalls;  // applies per mask so far (the capture is the second one: lazy setup done)
@@ -345,7 +346,7 @@ fda::GTrans make_items(fda_plan P, GroupedPairs& G, const std::vector<int64_t>& 
   const int cols = fda::gtrans_cols(T);
   const double ppg = (double)np / (double)std::max<int64_t>(ng, 1);
   // FDA_GT_MODE=atomic|owned|auto forces the item kind (experiments); FDA_GT_CHUNK: pairs per atomic item
-  const char* gm = mode ? mode : getenv("FDA_GT_MODE");
+  const char* gm = P->deterministic ? "owned" : mode ? mode : getenv("FDA_GT_MODE");
   // Default: group-major items of <= 1024 pairs with atomic accumulation (measured at config 5: 400 ms
   // apply vs 440 ms with the automatic choice and 509 ms with owned items only; 1024 vs 256 pairs:
   // 332 vs 336 ms).
@@ -765,6 +766,7 @@ fda_status upload_plan(fda_plan P, const fda_options& o) {
   fda::HostPlan& H = P->H;
   const int64_t n = H.n;
   P->n = n;
+  P->deterministic = o.deterministic != 0;
   if (!P->px) {  // host-built tree (the device tree leaves the Morton-ordered geometry in place)
     P->px = upload(P, H.px), P->py = upload(P, H.py), P->pz = upload(P, H.pz);
     P->nx = upload(P, H.nx), P->ny = upload(P, H.ny), P->nz = upload(P, H.nz);
@@ -1412,6 +1414,7 @@ void fda_options_default(fda_options* o) {
   o->nranks = 1;
   o->verbose = 0;
   o->graph = 1;
+  o->deterministic = 0;
 }
 
 const char* fda_status_str(fda_status s) {
@@ -1737,7 +1740,7 @@ void stage_near(fda_plan P, uint32_t mask, cudaStream_t st, Marks& mk) {
   const bool partial = P->leaf_b > 0 || P->leaf_e < P->nleaf;
   mk.begin(1);
   // symmetric P2P (each leaf pair once, both directions; BM_H on a single-rank plan; FDA_P2P_SYM=0: off)
-  const bool sym = (mask & FDA_PHASE_NEAR) && !partial && P->kind == 0 &&
+  const bool sym = (mask & FDA_PHASE_NEAR) && !partial && P->kind == 0 && !P->deterministic &&
                    !(getenv("FDA_P2P_SYM") && getenv("FDA_P2P_SYM")[0] == '0');
   if (!(mask & FDA_PHASE_NEAR) || partial || sym) ck(cudaMemsetAsync(P->outm, 0, (size_t)P->n * sizeof(double2), st));
   if (sym)

@@ -41,7 +41,7 @@ class fda_options(ctypes.Structure):
                 ("single_leaf", ctypes.c_int32), ("hf_max_rows", ctypes.c_int32), ("hf_spacing", ctypes.c_double),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("verbose", ctypes.c_int32),
                 ("eps_lowrank", ctypes.c_double), ("kernel", ctypes.c_int32), ("host_only", ctypes.c_int32),
-                ("original", ctypes.c_int32), ("graph", ctypes.c_int32)]
+                ("original", ctypes.c_int32), ("graph", ctypes.c_int32), ("deterministic", ctypes.c_int32)]
 
 
 class fda_stats(ctypes.Structure):
